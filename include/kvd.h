@@ -1,0 +1,259 @@
+/*
+ * kvd.h -- C ABI of the B200-native paged-KV pull (KVDirect, arXiv 2501.14743).
+ *
+ * The library moves a finished prefill request's paged KV cache into a
+ * decode worker's paged KV cache by PULLING it: one kernel, launched on the
+ * decode GPU, loads the source blocks straight out of the prefill GPU's HBM
+ * over NVLink 5 / NVSwitch (CUDA IPC mapping) and stores them into the
+ * decode cache's blocks, for every layer and both K and V, then raises a
+ * per-request completion flag the host polls (§4.3 pull mode,
+ * P:L404 "pull-mode performs KV cache reads for all layers in a single
+ * shot"; §4.1 Connect/Transfer/Complete).
+ *
+ * Citations: P:Lnnn = line nnn of the paper's source.
+ *
+ * Conventions for every entry point
+ *   - Return a kvd_status; 0 is success, negative is an error.  No entry
+ *     point aborts or throws across the ABI.  kvd_last_error() returns a
+ *     thread-local detail string for the most recent failure on the thread.
+ *   - Pointers named *_dev are device pointers (CUDA global memory); all
+ *     other pointers are host pointers.  `stream` is a cudaStream_t passed
+ *     as void* (NULL = legacy default stream) of the device that owns the
+ *     decode-side cache.
+ *   - Host arrays (block ids, blobs) are borrowed for the duration of the
+ *     call only; the library copies what it keeps.
+ *   - Every entry point saves and restores the calling thread's current
+ *     CUDA device.
+ *   - Entry points marked [host-only] make no CUDA call and work on a
+ *     machine without a GPU.
+ */
+#ifndef KVD_H
+#define KVD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KVD_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define KVD_API __attribute__((visibility("default")))
+#else
+#define KVD_API
+#endif
+
+typedef enum {
+  KVD_OK = 0,
+  KVD_EINVAL = -1,   /* bad argument: null pointer, duplicate destination id, unknown request */
+  KVD_ERANGE = -2,   /* a block id outside [0, num_blocks) of its side */
+  KVD_ELAYOUT = -3,  /* unsupported / incompatible / misaligned layout */
+  KVD_EHANDLE = -4,  /* IPC export or import failed, malformed blob */
+  KVD_ECUDA = -5,    /* a CUDA runtime call failed (detail in kvd_last_error) */
+  KVD_ENOMEM = -6,   /* host or device allocation failed */
+  KVD_EBUSY = -7,    /* request id already in flight on this peer, or no free completion slot */
+  KVD_ESTATE = -8    /* object used in the wrong state (e.g. closed) */
+} kvd_status;
+
+/* Element type of the cache.  Only its size matters: the pull is a bit copy. */
+typedef enum { KVD_FP16 = 0, KVD_BF16 = 1, KVD_FP8 = 2, KVD_FP32 = 3 } kvd_dtype;
+
+/*
+ * Tensor-centric metadata of one side's paged KV cache (Fig. 5).
+ * vLLM keeps one tensor per layer; all layers share this layout.  The
+ * logical tensor is cache[B][KV][L][H][D]: B = num_blocks,
+ * KV = 2 (K and V), L = block_size tokens, H = num_kv_heads (per shard),
+ * D = head_dim.  `stride` holds ELEMENT strides in that Dims order; all
+ * zeros selects Fig. 5's layout, stride = (L*H*D, B*L*H*D, H*D, D, 1),
+ * i.e. vLLM's flash layout (2, num_blocks, block_size, heads, head_dim).
+ * Requirements (else KVD_ELAYOUT): strides > 0; the (L, H, D) sub-tensor of
+ * a block is self-contiguous (reading R4); the element offsets of
+ * distinct (B, KV) pairs do not overlap; span and byte strides are
+ * multiples of 16 bytes.
+ */
+typedef struct {
+  uint32_t num_layers;
+  uint32_t num_kv_heads;
+  uint32_t head_dim;
+  uint32_t block_size;
+  uint32_t num_blocks;
+  uint32_t dtype;        /* kvd_dtype */
+  int64_t stride[5];     /* element strides, Dims order (B, KV, L, H, D) */
+} kvd_layout;
+
+/* Byte geometry derived from a kvd_layout. */
+typedef struct {
+  uint64_t span_bytes;          /* one (block, K|V) sub-tensor: "shape x stride" */
+  int64_t block_stride_bytes;   /* e * stride[B] */
+  int64_t plane_stride_bytes;   /* e * stride[KV] */
+  uint64_t layer_bytes;         /* bytes one layer tensor spans from its base */
+  uint32_t elem_bytes;
+  uint32_t kv_adjacent;         /* 1 if plane_stride == span: K,V of a block are one 2*span unit */
+} kvd_geometry;
+
+/* A coalesced run: blocks src_start+j -> dst_start+j for j < len. */
+typedef struct {
+  int32_t src_start;
+  int32_t dst_start;
+  uint32_t len;
+} kvd_run;
+
+/* What the most recent kvd_pull on a peer did (for benchmarks and tests). */
+typedef struct {
+  uint64_t request_id;
+  uint64_t bytes;        /* algorithmic bytes moved: n * layers * 2 * span */
+  uint32_t blocks;       /* n */
+  uint32_t runs;         /* coalesced runs m (<= n) */
+  uint64_t segments;     /* contiguous byte segments: layers * planes * (runs or blocks) */
+  uint64_t tiles;        /* warp work items */
+  uint32_t ctas;         /* grid size */
+  uint32_t threads;      /* threads per CTA */
+  uint32_t variant;      /* kvd_variant actually launched */
+  uint32_t launches;     /* kernels (or copies) issued by the call */
+} kvd_pull_info;
+
+typedef enum {
+  KVD_VARIANT_AUTO = 0,  /* library choice */
+  KVD_VARIANT_LSU = 1,   /* SM loads 16 B/lane from the peer, stores locally (default) */
+  KVD_VARIANT_LSU32 = 2, /* 32 B/lane (sm_100 256-bit ld/st); needs 32 B alignment */
+  KVD_VARIANT_CE = 3     /* copy engine: one cudaMemcpyAsync per segment (comparator only) */
+} kvd_variant;
+
+typedef enum {
+  KVD_OPT_MAX_CTAS = 0,     /* cap on the pull grid (default: SMs * resident CTAs/SM) */
+  KVD_OPT_TILE_BYTES = 1,   /* bytes per warp work item, multiple of 512 (default 16384) */
+  KVD_OPT_COALESCE = 2,     /* 1 (default) merge bi-contiguous runs; 0 one run per block (E10 ablation) */
+  KVD_OPT_VARIANT = 3,      /* kvd_variant */
+  KVD_OPT_THREADS = 4       /* threads per CTA: 128..1024, multiple of 32 (default 512) */
+} kvd_option;
+
+typedef struct kvd_cache_s* kvd_cache;
+typedef struct kvd_peer_s* kvd_peer;
+
+/* ---------------------------------------------------------------------------
+ * Host-only helpers (row a1 / a3 of the design; usable without a GPU)
+ * ------------------------------------------------------------------------- */
+
+/* [host-only] Validate a layout and derive its byte geometry.
+ * Errors: KVD_EINVAL (null), KVD_ELAYOUT (see kvd_layout requirements). */
+KVD_API kvd_status kvd_layout_geometry(const kvd_layout* layout, kvd_geometry* out);
+
+/* [host-only] Validate a block table and coalesce it into maximal runs
+ * (merge consecutive entries only when both the remote and the
+ * local blocks continue the previous ones).  src_ids/dst_ids: n entries;
+ * ids must lie in [0, src_num_blocks) / [0, dst_num_blocks) (else
+ * KVD_ERANGE) and dst ids must be distinct (else KVD_EINVAL).  coalesce=0
+ * emits one run per entry.  Writes at most `cap` runs to `runs` and the run
+ * count to *m; KVD_ENOMEM if cap is too small (then *m is the count needed). */
+KVD_API kvd_status kvd_plan(const int32_t* src_ids, const int32_t* dst_ids, uint32_t n,
+                    uint32_t src_num_blocks, uint32_t dst_num_blocks, int coalesce,
+                    kvd_run* runs, uint32_t cap, uint32_t* m);
+
+/* [host-only] Decode an export blob's header without opening it.
+ * Any out pointer may be NULL.  KVD_EHANDLE on a malformed blob. */
+KVD_API kvd_status kvd_blob_info(const void* blob, size_t blob_len, kvd_layout* layout,
+                         int32_t* device, int64_t* pid, uint32_t* num_allocations);
+
+/* ---------------------------------------------------------------------------
+ * Row a1: register a cache (both sides, once)
+ * ------------------------------------------------------------------------- */
+
+/* Register the paged cache whose layer l starts at device address
+ * layer_base_dev[l] (num_layers entries) on CUDA device `device`.
+ * The caller keeps ownership of the memory and must keep it alive until
+ * kvd_unregister_cache and, for an exporter, until every importer has
+ * closed its peer (CUDA IPC rule).  Bases must be 16 B aligned and each
+ * layer's extent must lie inside one allocation (checked when a GPU is
+ * present).  Errors: KVD_EINVAL, KVD_ELAYOUT, KVD_ECUDA, KVD_ENOMEM. */
+KVD_API kvd_status kvd_register_cache(int device, const kvd_layout* layout,
+                              void* const* layer_base_dev, kvd_cache* out);
+
+KVD_API kvd_status kvd_unregister_cache(kvd_cache cache);
+
+/* ---------------------------------------------------------------------------
+ * Row a2: one-time tensor-centric exchange (Connect())
+ * ------------------------------------------------------------------------- */
+
+/* Serialise the cache's metadata -- layout (Address/Dims/Shape/Stride,
+ * P:L294) plus one CUDA IPC handle per distinct allocation and each layer's
+ * (allocation, offset) -- into the caller's buffer.  *blob_len: in =
+ * capacity, out = bytes written (or needed, with KVD_ENOMEM).  The blob is
+ * plain bytes; ship it to the decode process any way (torch.distributed,
+ * TCPStore, socket).  Errors: KVD_EINVAL, KVD_ENOMEM, KVD_EHANDLE
+ * (memory not legacy-IPC capable, e.g. VMM/expandable segments). */
+KVD_API kvd_status kvd_export_handle(kvd_cache cache, void* blob, size_t* blob_len);
+
+/* Import a prefill cache's blob on the decode side and bind it to the local
+ * destination cache.  Checks compatibility (same layers, heads, head_dim,
+ * block_size, element size; B/KV strides and num_blocks may differ)
+ * -> KVD_ELAYOUT; maps each allocation with cudaIpcOpenMemHandle on the
+ * local device (or, for a blob exported by this same process, uses the raw
+ * pointers and enables peer access) -> KVD_EHANDLE / KVD_ECUDA.
+ * Allocates the completion-slot ring (pinned mapped host flags). */
+KVD_API kvd_status kvd_open_peer(kvd_cache local_dst, const void* blob, size_t blob_len,
+                         kvd_peer* out);
+
+KVD_API kvd_status kvd_close_peer(kvd_peer peer);
+
+/* Tune a peer (see kvd_option).  KVD_EINVAL on an unknown option/value. */
+KVD_API kvd_status kvd_peer_set(kvd_peer peer, int option, int64_t value);
+
+/* ---------------------------------------------------------------------------
+ * Rows a3-a6: the per-request pull (Transfer() x n + Complete())
+ * ------------------------------------------------------------------------- */
+
+/* Pull request `request_id`: for every i < n, every layer and K and V,
+ * copy remote block src_ids[i] of the prefill cache into local block
+ * dst_ids[i] of the decode cache, bit for bit.  Validates (KVD_ERANGE,
+ * KVD_EINVAL) and coalesces on the host, then issues exactly ONE kernel
+ * launch on `stream` ("post ... without block") and returns without
+ * waiting.  On any error nothing is launched and no byte changes.
+ * request_id must not be in flight on this peer (KVD_EBUSY).  n = 0 is
+ * valid: a flag-only launch; the request completes with no bytes moved. */
+KVD_API kvd_status kvd_pull(kvd_peer peer, uint64_t request_id, const int32_t* src_ids,
+                    const int32_t* dst_ids, uint32_t n, void* stream);
+
+/* Non-blocking completion check (Complete()): *done = 1
+ * once every byte of the request has landed in decode HBM and is visible
+ * to later work on the decode GPU and to the host; the request is then
+ * retired (its id may be reused; a later poll of it returns KVD_EINVAL).
+ * *done = 0 while in flight.  Makes no CUDA call (reads a pinned flag).
+ * Errors: KVD_EINVAL for an unknown request id. */
+KVD_API kvd_status kvd_poll_done(kvd_peer peer, uint64_t request_id, int* done);
+
+/* Spin on kvd_poll_done until done or `timeout_us` elapses (KVD_EBUSY). */
+KVD_API kvd_status kvd_wait_done(kvd_peer peer, uint64_t request_id, int64_t timeout_us);
+
+/* Describe the most recent kvd_pull on this peer. */
+KVD_API kvd_status kvd_last_pull_info(kvd_peer peer, kvd_pull_info* out);
+
+/* ---------------------------------------------------------------------------
+ * Message-passing baseline helpers (fig:diff(a): gather kernel ->
+ * send -> receive -> scatter kernel).  Used only by the NCCL comparator.
+ * Staging layout: [layer][kv][i][span] -- n blocks of every (layer, K|V)
+ * packed back to back; staging_dev holds layers * 2 * n * span bytes.
+ * ------------------------------------------------------------------------- */
+
+/* Gather cache blocks ids[0..n) into staging_dev (one launch on stream). */
+KVD_API kvd_status kvd_gather(kvd_cache cache, const int32_t* ids, uint32_t n, void* staging_dev,
+                      void* stream);
+
+/* Scatter staging_dev into cache blocks ids[0..n) (one launch on stream). */
+KVD_API kvd_status kvd_scatter(kvd_cache cache, const int32_t* ids, uint32_t n,
+                       const void* staging_dev, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Diagnostics
+ * ------------------------------------------------------------------------- */
+
+KVD_API const char* kvd_strerror(kvd_status status);
+KVD_API const char* kvd_last_error(void);
+KVD_API int kvd_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KVD_H */

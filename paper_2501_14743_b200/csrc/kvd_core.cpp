@@ -1,0 +1,1002 @@
+// kvd_core.cpp -- host core of the paged-KV pull library (include/kvd.h).
+//
+// Rows of the design this file implements (SURVEY.md §8 / DESIGN.md):
+//   a1  cache registration and layout normalisation
+//   a2  export / open: the one-time tensor-centric exchange over CUDA IPC
+//       (Connect())
+//   a3  block-table validation and run coalescing
+//   a4  descriptor staging and the single launch
+//   a6  completion slots and kvd_poll_done
+// The kernel itself (a5) lives in kvd_pull.cu.
+#include "../../include/kvd.h"
+
+#include <cuda_runtime.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <random>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "kvd_internal.h"
+
+// ===========================================================================
+// errors
+// ===========================================================================
+namespace {
+
+thread_local std::string g_last_error;
+
+kvd_status fail(kvd_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return s;
+}
+
+kvd_status cuda_fail(cudaError_t e, const char* what) {
+  return fail(KVD_ECUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+#define KVD_CUDA(call)                                  \
+  do {                                                  \
+    cudaError_t _e = (call);                            \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call); \
+  } while (0)
+
+// Saves and restores the calling thread's current device (the caller may be
+// PyTorch with its own notion of the current device).
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = false;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    ok = (prev == dev) || (cudaSetDevice(dev) == cudaSuccess);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+uint64_t process_nonce() {
+  static const uint64_t nonce = [] {
+    std::random_device rd;
+    return (static_cast<uint64_t>(rd()) << 32) ^ rd() ^
+           static_cast<uint64_t>(std::chrono::steady_clock::now().time_since_epoch().count());
+  }();
+  return nonce;
+}
+
+uint32_t elem_size(uint32_t dtype) {
+  switch (dtype) {
+    case KVD_FP16: return 2;
+    case KVD_BF16: return 2;
+    case KVD_FP8: return 1;
+    case KVD_FP32: return 4;
+    default: return 0;
+  }
+}
+
+// ===========================================================================
+// a1: layout -> geometry
+// ===========================================================================
+enum { kB = 0, kKV = 1, kL = 2, kH = 3, kD = 4 };
+
+struct Geom {
+  kvd_layout layout;       // with resolved (non-zero) strides
+  kvd_geometry g;
+};
+
+// Fig. 5's layout for the given shape.
+void default_strides(const kvd_layout& L, int64_t s[5]) {
+  const int64_t sub = (int64_t)L.block_size * L.num_kv_heads * L.head_dim;
+  s[kB] = sub;
+  s[kKV] = (int64_t)L.num_blocks * sub;
+  s[kL] = (int64_t)L.num_kv_heads * L.head_dim;
+  s[kH] = L.head_dim;
+  s[kD] = 1;
+}
+
+kvd_status make_geom(const kvd_layout* in, Geom* out) {
+  if (!in || !out) return fail(KVD_EINVAL, "null layout");
+  kvd_layout L = *in;
+  const uint32_t e = elem_size(L.dtype);
+  if (!e) return fail(KVD_ELAYOUT, "unknown dtype %u", L.dtype);
+  if (!L.num_layers || !L.num_kv_heads || !L.head_dim || !L.block_size || !L.num_blocks)
+    return fail(KVD_ELAYOUT, "zero extent in layout");
+  if (L.num_blocks > 0x7fffffffu) return fail(KVD_ELAYOUT, "num_blocks exceeds int32");
+  bool all_zero = true;
+  for (int k = 0; k < 5; ++k) all_zero = all_zero && L.stride[k] == 0;
+  if (all_zero) default_strides(L, L.stride);
+  for (int k = 0; k < 5; ++k)
+    if (L.stride[k] <= 0) return fail(KVD_ELAYOUT, "stride[%d] must be > 0", k);
+
+  // (L, H, D) sub-tensor must be self-contiguous (reading R4): ignoring
+  // extent-1 dims, the strides sorted ascending form the chain 1, n0, n0*n1.
+  struct DS { int64_t stride, shape; };
+  DS inner[3] = {{L.stride[kL], L.block_size}, {L.stride[kH], L.num_kv_heads},
+                 {L.stride[kD], L.head_dim}};
+  std::vector<DS> v;
+  for (auto& d : inner)
+    if (d.shape > 1) v.push_back(d);
+  std::sort(v.begin(), v.end(), [](const DS& a, const DS& b) { return a.stride < b.stride; });
+  int64_t expect = 1;
+  for (auto& d : v) {
+    if (d.stride != expect)
+      return fail(KVD_ELAYOUT, "(L,H,D) sub-tensor is not self-contiguous (stride %lld, expected %lld)",
+                  (long long)d.stride, (long long)expect);
+    expect *= d.shape;
+  }
+  const int64_t sub = (int64_t)L.block_size * L.num_kv_heads * L.head_dim;
+  const int64_t sB = L.stride[kB], sKV = L.stride[kKV];
+  const int64_t NB = L.num_blocks;
+  // (block, kv) units must not overlap: K/V planes outside the blocks
+  // (Fig. 5), or K and V inside each block (block-major).
+  const bool kv_outer = sB >= sub && sKV >= (NB - 1) * sB + sub;
+  const bool kv_inner = sKV >= sub && sB >= sKV + sub;
+  if (!kv_outer && !kv_inner)
+    return fail(KVD_ELAYOUT, "(B, KV) strides %lld, %lld overlap the %lld-element block tensors",
+                (long long)sB, (long long)sKV, (long long)sub);
+  kvd_geometry g{};
+  g.elem_bytes = e;
+  g.span_bytes = (uint64_t)sub * e;
+  g.block_stride_bytes = sB * e;
+  g.plane_stride_bytes = sKV * e;
+  g.layer_bytes = (uint64_t)(((NB - 1) * sB + sKV) * e) + g.span_bytes;
+  g.kv_adjacent = (uint64_t)g.plane_stride_bytes == g.span_bytes ? 1u : 0u;
+  if (g.span_bytes % 16 || g.block_stride_bytes % 16 || g.plane_stride_bytes % 16)
+    return fail(KVD_ELAYOUT, "span and byte strides must be multiples of 16 B");
+  out->layout = L;
+  out->g = g;
+  return KVD_OK;
+}
+
+// ===========================================================================
+// a3: validate + coalesce
+// ===========================================================================
+struct Planner {
+  std::vector<uint32_t> stamp;   // dst id -> epoch of last use (duplicate check)
+  uint32_t epoch = 0;
+
+  kvd_status plan(const int32_t* src, const int32_t* dst, uint32_t n, uint32_t src_nb,
+                  uint32_t dst_nb, bool coalesce, std::vector<kvd_run>& runs) {
+    runs.clear();
+    if (n && (!src || !dst)) return fail(KVD_EINVAL, "null block id array");
+    if (stamp.size() < dst_nb) stamp.assign(dst_nb, 0u);
+    if (++epoch == 0) {
+      std::fill(stamp.begin(), stamp.end(), 0u);
+      epoch = 1;
+    }
+    for (uint32_t i = 0; i < n; ++i) {
+      const int32_t s = src[i], d = dst[i];
+      if (s < 0 || (uint32_t)s >= src_nb)
+        return fail(KVD_ERANGE, "src_ids[%u] = %d outside [0, %u)", i, s, src_nb);
+      if (d < 0 || (uint32_t)d >= dst_nb)
+        return fail(KVD_ERANGE, "dst_ids[%u] = %d outside [0, %u)", i, d, dst_nb);
+      if (stamp[d] == epoch) return fail(KVD_EINVAL, "duplicate destination block %d", d);
+      stamp[d] = epoch;
+      if (coalesce && !runs.empty()) {
+        kvd_run& r = runs.back();
+        if (s == r.src_start + (int32_t)r.len && d == r.dst_start + (int32_t)r.len) {
+          ++r.len;
+          continue;
+        }
+      }
+      runs.push_back(kvd_run{s, d, 1u});
+    }
+    return KVD_OK;
+  }
+};
+
+// ===========================================================================
+// a2: blob codec (little-endian, fixed width)
+// ===========================================================================
+constexpr uint32_t kMagic = 0x4244564bu;  // "KVDB"
+constexpr uint32_t kBlobVersion = 1;
+
+struct BlobAlloc {
+  cudaIpcMemHandle_t handle;
+  uint64_t base;     // exporter's virtual address (same-process import)
+  uint64_t size;
+};
+struct BlobLayer {
+  uint32_t alloc;
+  uint64_t offset;
+};
+struct Blob {
+  int32_t device = -1;
+  int64_t pid = 0;
+  uint64_t nonce = 0;
+  kvd_layout layout{};
+  std::vector<BlobAlloc> allocs;
+  std::vector<BlobLayer> layers;
+};
+
+struct Writer {
+  std::vector<uint8_t> b;
+  void u32(uint32_t v) { for (int i = 0; i < 4; ++i) b.push_back((uint8_t)(v >> (8 * i))); }
+  void u64(uint64_t v) { for (int i = 0; i < 8; ++i) b.push_back((uint8_t)(v >> (8 * i))); }
+  void raw(const void* p, size_t n) { b.insert(b.end(), (const uint8_t*)p, (const uint8_t*)p + n); }
+};
+struct Reader {
+  const uint8_t* p;
+  size_t n, i = 0;
+  bool ok = true;
+  bool need(size_t k) { if (i + k > n) ok = false; return ok; }
+  uint32_t u32() { if (!need(4)) return 0; uint32_t v = 0; for (int k = 0; k < 4; ++k) v |= (uint32_t)p[i++] << (8 * k); return v; }
+  uint64_t u64() { if (!need(8)) return 0; uint64_t v = 0; for (int k = 0; k < 8; ++k) v |= (uint64_t)p[i++] << (8 * k); return v; }
+  void raw(void* dst, size_t k) { if (!need(k)) return; memcpy(dst, p + i, k); i += k; }
+};
+
+std::vector<uint8_t> encode_blob(const Blob& B) {
+  Writer w;
+  w.u32(kMagic);
+  w.u32(kBlobVersion);
+  w.u32((uint32_t)B.device);
+  w.u32(0);
+  w.u64((uint64_t)B.pid);
+  w.u64(B.nonce);
+  const kvd_layout& L = B.layout;
+  w.u32(L.num_layers); w.u32(L.num_kv_heads); w.u32(L.head_dim);
+  w.u32(L.block_size); w.u32(L.num_blocks); w.u32(L.dtype);
+  for (int k = 0; k < 5; ++k) w.u64((uint64_t)L.stride[k]);
+  w.u32((uint32_t)B.allocs.size());
+  w.u32((uint32_t)B.layers.size());
+  for (auto& a : B.allocs) {
+    w.raw(&a.handle, sizeof(a.handle));
+    w.u64(a.base);
+    w.u64(a.size);
+  }
+  for (auto& l : B.layers) {
+    w.u32(l.alloc);
+    w.u32(0);
+    w.u64(l.offset);
+  }
+  w.u32(kMagic);  // trailer
+  return w.b;
+}
+
+kvd_status decode_blob(const void* data, size_t len, Blob* B) {
+  if (!data) return fail(KVD_EINVAL, "null blob");
+  Reader r{(const uint8_t*)data, len};
+  if (r.u32() != kMagic) return fail(KVD_EHANDLE, "blob: bad magic");
+  if (r.u32() != kBlobVersion) return fail(KVD_EHANDLE, "blob: unsupported version");
+  B->device = (int32_t)r.u32();
+  r.u32();
+  B->pid = (int64_t)r.u64();
+  B->nonce = r.u64();
+  kvd_layout& L = B->layout;
+  L.num_layers = r.u32(); L.num_kv_heads = r.u32(); L.head_dim = r.u32();
+  L.block_size = r.u32(); L.num_blocks = r.u32(); L.dtype = r.u32();
+  for (int k = 0; k < 5; ++k) L.stride[k] = (int64_t)r.u64();
+  const uint32_t na = r.u32(), nl = r.u32();
+  if (!r.ok) return fail(KVD_EHANDLE, "blob: truncated header");
+  if (nl != L.num_layers || na == 0 || na > nl)
+    return fail(KVD_EHANDLE, "blob: inconsistent counts (%u allocations, %u layers)", na, nl);
+  if ((size_t)na * (sizeof(cudaIpcMemHandle_t) + 16) + (size_t)nl * 16 + 4 > len - r.i)
+    return fail(KVD_EHANDLE, "blob: truncated body");
+  B->allocs.resize(na);
+  for (auto& a : B->allocs) {
+    r.raw(&a.handle, sizeof(a.handle));
+    a.base = r.u64();
+    a.size = r.u64();
+  }
+  B->layers.resize(nl);
+  for (auto& l : B->layers) {
+    l.alloc = r.u32();
+    r.u32();
+    l.offset = r.u64();
+    if (l.alloc >= na) return fail(KVD_EHANDLE, "blob: layer references allocation %u", l.alloc);
+  }
+  if (r.u32() != kMagic || !r.ok) return fail(KVD_EHANDLE, "blob: bad trailer");
+  return KVD_OK;
+}
+
+// ===========================================================================
+// driver entry point (no link-time dependency on libcuda)
+// ===========================================================================
+typedef int (*PFN_memGetAddressRange)(unsigned long long*, size_t*, unsigned long long);
+
+PFN_memGetAddressRange get_address_range_fn() {
+  static PFN_memGetAddressRange fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) !=
+            cudaSuccess || q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return (PFN_memGetAddressRange)p;
+  }();
+  return fn;
+}
+
+// ===========================================================================
+// IPC mapping registry: a handle may be opened once per device per process
+// ===========================================================================
+struct Mapping {
+  void* ptr = nullptr;
+  int refs = 0;
+};
+std::mutex g_map_mu;
+std::map<std::pair<std::string, int>, Mapping> g_mappings;
+
+kvd_status ipc_open(const cudaIpcMemHandle_t& h, int device, void** out) {
+  std::lock_guard<std::mutex> lk(g_map_mu);
+  auto key = std::make_pair(std::string((const char*)&h, sizeof(h)), device);
+  auto it = g_mappings.find(key);
+  if (it != g_mappings.end()) {
+    ++it->second.refs;
+    *out = it->second.ptr;
+    return KVD_OK;
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(KVD_EHANDLE, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+  }
+  g_mappings[key] = Mapping{p, 1};
+  *out = p;
+  return KVD_OK;
+}
+
+void ipc_close(const cudaIpcMemHandle_t& h, int device) {
+  std::lock_guard<std::mutex> lk(g_map_mu);
+  auto key = std::make_pair(std::string((const char*)&h, sizeof(h)), device);
+  auto it = g_mappings.find(key);
+  if (it == g_mappings.end()) return;
+  if (--it->second.refs == 0) {
+    cudaIpcCloseMemHandle(it->second.ptr);
+    g_mappings.erase(it);
+  }
+}
+
+}  // namespace
+
+// ===========================================================================
+// objects
+// ===========================================================================
+struct kvd_cache_s {
+  int device = -1;
+  Geom geom;
+  std::vector<uint64_t> bases;            // layer base addresses
+  unsigned long long* d_bases = nullptr;  // device copy of bases
+  std::mutex mu;
+  Planner planner;                        // for gather/scatter
+  std::vector<kvd_run> runs;
+  std::vector<int4> runs4;
+  std::vector<int32_t> iota;
+};
+
+namespace {
+constexpr uint32_t kSlots = 1024;
+}
+
+struct kvd_peer_s {
+  kvd_cache local = nullptr;
+  Geom remote;
+  int remote_device = -1;
+  bool same_process = false;
+  std::vector<cudaIpcMemHandle_t> opened;  // handles we opened (to close)
+  unsigned long long* d_src_bases = nullptr;
+  std::vector<uint64_t> src_bases;         // host copy of the mapped remote layer bases
+
+  // completion slots (a6)
+  unsigned long long* flags = nullptr;      // pinned, host-mapped
+  unsigned long long* flags_dev = nullptr;
+  unsigned int* counters = nullptr;         // device
+  std::vector<uint64_t> slot_seq;           // 0 = free, else the token in flight
+  uint32_t cursor = 0;
+  uint64_t seq = 0;
+  std::unordered_map<uint64_t, std::pair<uint32_t, uint64_t>> inflight;  // req -> (slot, token)
+  std::vector<int4*> slot_runs_dev;         // big run tables (per slot)
+  std::vector<uint32_t> slot_runs_cap;
+  std::vector<int4*> slot_runs_host;        // pinned staging for the above
+
+  // options
+  uint32_t max_ctas = 0;
+  uint32_t tile_bytes = 16384;
+  uint32_t threads = 512;
+  int coalesce = 1;
+  int variant = KVD_VARIANT_AUTO;
+  int sm_count = 148;
+
+  std::mutex mu;
+  Planner planner;
+  std::vector<kvd_run> runs;
+  std::vector<int4> runs4;
+  kvd_pull_info last{};
+  bool closed = false;
+};
+
+// ===========================================================================
+// shared launch planning (a4)
+// ===========================================================================
+namespace {
+
+struct PairPlan {
+  uint32_t planes;
+  uint64_t unit;
+  bool contiguous;
+};
+
+PairPlan pair_plan(const kvd_geometry& s, const kvd_geometry& d) {
+  PairPlan p;
+  if (s.kv_adjacent && d.kv_adjacent) {
+    p.planes = 1;
+    p.unit = 2 * s.span_bytes;
+  } else {
+    p.planes = 2;
+    p.unit = s.span_bytes;
+  }
+  p.contiguous = (uint64_t)s.block_stride_bytes == p.unit &&
+                 (uint64_t)d.block_stride_bytes == p.unit;
+  return p;
+}
+
+// Fill runs4 (= runs + tile prefix) and the tiling fields of args.
+kvd_status tile_runs(const std::vector<kvd_run>& runs, const PairPlan& pp, uint32_t num_layers,
+                     uint32_t tile_bytes, std::vector<int4>& runs4, kvd::PullArgs& a) {
+  runs4.resize(runs.size());
+  const uint64_t tpu = (pp.unit + tile_bytes - 1) / tile_bytes;
+  uint64_t acc = 0;
+  for (size_t r = 0; r < runs.size(); ++r) {
+    const uint64_t t = pp.contiguous ? ((uint64_t)runs[r].len * pp.unit + tile_bytes - 1) / tile_bytes
+                                     : (uint64_t)runs[r].len * tpu;
+    acc += t;
+    if (acc >= 0x7fffffffull) return fail(KVD_ERANGE, "request too large for one launch");
+    runs4[r] = make_int4(runs[r].src_start, runs[r].dst_start, (int)runs[r].len, (int)acc);
+  }
+  const uint64_t total = acc * num_layers * pp.planes;
+  if (total >= 0x7fffffffull) return fail(KVD_ERANGE, "request too large for one launch");
+  a.unit_bytes = pp.unit;
+  a.num_layers = num_layers;
+  a.planes = pp.planes;
+  a.tile_bytes = tile_bytes;
+  a.contiguous = pp.contiguous ? 1u : 0u;
+  a.tiles_per_unit = (unsigned)tpu;
+  a.nruns = (unsigned)runs.size();
+  a.tiles_per_lp = (unsigned)acc;
+  a.total_tiles = (unsigned)total;
+  return KVD_OK;
+}
+
+bool aligned32(const kvd::PullArgs& a, const std::vector<uint64_t>& src_bases,
+               const std::vector<uint64_t>& dst_bases) {
+  if (a.unit_bytes % 32 || a.tile_bytes % 32) return false;
+  if (a.src.plane_stride % 32 || a.dst.plane_stride % 32) return false;
+  if (a.src.block_stride % 32 || a.dst.block_stride % 32) return false;
+  if (a.src.step % 32 || a.dst.step % 32 || a.src.base % 32 || a.dst.base % 32) return false;
+  for (auto b : src_bases) if (b % 32) return false;
+  for (auto b : dst_bases) if (b % 32) return false;
+  return true;
+}
+
+uint32_t grid_for(uint64_t total_tiles, uint32_t threads, uint32_t max_ctas) {
+  const uint32_t wpc = threads / 32;
+  uint64_t need = (total_tiles + wpc - 1) / wpc;
+  if (need < 1) need = 1;
+  return (uint32_t)std::min<uint64_t>(need, max_ctas);
+}
+
+}  // namespace
+
+// ===========================================================================
+// ABI: host-only helpers
+// ===========================================================================
+extern "C" {
+
+int kvd_abi_version(void) { return KVD_ABI_VERSION; }
+
+const char* kvd_strerror(kvd_status s) {
+  switch (s) {
+    case KVD_OK: return "ok";
+    case KVD_EINVAL: return "invalid argument";
+    case KVD_ERANGE: return "block id out of range";
+    case KVD_ELAYOUT: return "unsupported or incompatible layout";
+    case KVD_EHANDLE: return "IPC handle export/import failed";
+    case KVD_ECUDA: return "CUDA error";
+    case KVD_ENOMEM: return "out of memory / buffer too small";
+    case KVD_EBUSY: return "busy";
+    case KVD_ESTATE: return "invalid state";
+  }
+  return "unknown status";
+}
+
+const char* kvd_last_error(void) { return g_last_error.c_str(); }
+
+kvd_status kvd_layout_geometry(const kvd_layout* layout, kvd_geometry* out) {
+  if (!out) return fail(KVD_EINVAL, "null output");
+  Geom g;
+  kvd_status s = make_geom(layout, &g);
+  if (s != KVD_OK) return s;
+  *out = g.g;
+  return KVD_OK;
+}
+
+kvd_status kvd_plan(const int32_t* src_ids, const int32_t* dst_ids, uint32_t n,
+                    uint32_t src_num_blocks, uint32_t dst_num_blocks, int coalesce,
+                    kvd_run* runs, uint32_t cap, uint32_t* m) {
+  if (!m) return fail(KVD_EINVAL, "null run count");
+  Planner pl;
+  std::vector<kvd_run> v;
+  kvd_status s = pl.plan(src_ids, dst_ids, n, src_num_blocks, dst_num_blocks, coalesce != 0, v);
+  if (s != KVD_OK) return s;
+  *m = (uint32_t)v.size();
+  if (v.size() > cap) return fail(KVD_ENOMEM, "need %zu runs, capacity %u", v.size(), cap);
+  if (!v.empty()) {
+    if (!runs) return fail(KVD_EINVAL, "null run buffer");
+    memcpy(runs, v.data(), v.size() * sizeof(kvd_run));
+  }
+  return KVD_OK;
+}
+
+kvd_status kvd_blob_info(const void* blob, size_t blob_len, kvd_layout* layout, int32_t* device,
+                         int64_t* pid, uint32_t* num_allocations) {
+  Blob B;
+  kvd_status s = decode_blob(blob, blob_len, &B);
+  if (s != KVD_OK) return s;
+  if (layout) *layout = B.layout;
+  if (device) *device = B.device;
+  if (pid) *pid = B.pid;
+  if (num_allocations) *num_allocations = (uint32_t)B.allocs.size();
+  return KVD_OK;
+}
+
+// ===========================================================================
+// ABI: a1 register
+// ===========================================================================
+kvd_status kvd_register_cache(int device, const kvd_layout* layout, void* const* layer_base,
+                              kvd_cache* out) {
+  if (!out || !layout || !layer_base) return fail(KVD_EINVAL, "null argument");
+  *out = nullptr;
+  Geom g;
+  kvd_status s = make_geom(layout, &g);
+  if (s != KVD_OK) return s;
+  std::vector<uint64_t> bases(g.layout.num_layers);
+  for (uint32_t l = 0; l < g.layout.num_layers; ++l) {
+    bases[l] = (uint64_t)(uintptr_t)layer_base[l];
+    if (!bases[l]) return fail(KVD_EINVAL, "layer %u base is null", l);
+    if (bases[l] % 16) return fail(KVD_ELAYOUT, "layer %u base not 16 B aligned", l);
+  }
+  if (device < 0) return fail(KVD_EINVAL, "device %d", device);
+  DeviceGuard dg(device);
+  if (!dg.ok) return fail(KVD_ECUDA, "cannot select device %d", device);
+  // every layer's extent must lie inside one allocation
+  if (auto range = get_address_range_fn()) {
+    for (uint32_t l = 0; l < g.layout.num_layers; ++l) {
+      unsigned long long abase = 0;
+      size_t asize = 0;
+      if (range(&abase, &asize, (unsigned long long)bases[l]) != 0)
+        return fail(KVD_EINVAL, "layer %u base is not device memory", l);
+      if (bases[l] + g.g.layer_bytes > abase + asize)
+        return fail(KVD_ELAYOUT, "layer %u extent (%llu B) overruns its allocation", l,
+                    (unsigned long long)g.g.layer_bytes);
+    }
+  }
+  std::unique_ptr<kvd_cache_s> c(new (std::nothrow) kvd_cache_s());
+  if (!c) return fail(KVD_ENOMEM, "host allocation");
+  c->device = device;
+  c->geom = g;
+  c->bases = bases;
+  KVD_CUDA(cudaMalloc(&c->d_bases, bases.size() * sizeof(uint64_t)));
+  KVD_CUDA(cudaMemcpy(c->d_bases, bases.data(), bases.size() * sizeof(uint64_t),
+                      cudaMemcpyHostToDevice));
+  *out = c.release();
+  return KVD_OK;
+}
+
+kvd_status kvd_unregister_cache(kvd_cache c) {
+  if (!c) return fail(KVD_EINVAL, "null cache");
+  {
+    DeviceGuard dg(c->device);
+    if (c->d_bases) cudaFree(c->d_bases);
+  }
+  delete c;
+  return KVD_OK;
+}
+
+// ===========================================================================
+// ABI: a2 export / open
+// ===========================================================================
+kvd_status kvd_export_handle(kvd_cache c, void* blob, size_t* blob_len) {
+  if (!c || !blob_len) return fail(KVD_EINVAL, "null argument");
+  DeviceGuard dg(c->device);
+  if (!dg.ok) return fail(KVD_ECUDA, "cannot select device %d", c->device);
+  auto range = get_address_range_fn();
+  if (!range) return fail(KVD_ECUDA, "cuMemGetAddressRange entry point unavailable");
+  Blob B;
+  B.device = c->device;
+  B.pid = (int64_t)getpid();
+  B.nonce = process_nonce();
+  B.layout = c->geom.layout;
+  std::map<uint64_t, uint32_t> index;
+  for (uint32_t l = 0; l < c->bases.size(); ++l) {
+    unsigned long long abase = 0;
+    size_t asize = 0;
+    if (range(&abase, &asize, (unsigned long long)c->bases[l]) != 0)
+      return fail(KVD_EHANDLE, "layer %u: cuMemGetAddressRange failed", l);
+    auto it = index.find(abase);
+    if (it == index.end()) {
+      BlobAlloc a{};
+      cudaError_t e = cudaIpcGetMemHandle(&a.handle, (void*)(uintptr_t)abase);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(KVD_EHANDLE,
+                    "cudaIpcGetMemHandle(layer %u): %s -- memory must come from cudaMalloc "
+                    "(not VMM / expandable segments)", l, cudaGetErrorString(e));
+      }
+      a.base = abase;
+      a.size = asize;
+      it = index.emplace(abase, (uint32_t)B.allocs.size()).first;
+      B.allocs.push_back(a);
+    }
+    B.layers.push_back(BlobLayer{it->second, c->bases[l] - abase});
+  }
+  std::vector<uint8_t> bytes = encode_blob(B);
+  const size_t cap = *blob_len;
+  *blob_len = bytes.size();
+  if (!blob || cap < bytes.size())
+    return fail(KVD_ENOMEM, "blob needs %zu bytes, capacity %zu", bytes.size(), cap);
+  memcpy(blob, bytes.data(), bytes.size());
+  return KVD_OK;
+}
+
+static void peer_release(kvd_peer p) {
+  if (!p) return;
+  DeviceGuard dg(p->local ? p->local->device : 0);
+  for (auto& h : p->opened) ipc_close(h, p->local->device);
+  if (p->d_src_bases) cudaFree(p->d_src_bases);
+  if (p->flags) cudaFreeHost(p->flags);
+  if (p->counters) cudaFree(p->counters);
+  for (auto q : p->slot_runs_dev) if (q) cudaFree(q);
+  for (auto q : p->slot_runs_host) if (q) cudaFreeHost(q);
+  delete p;
+}
+
+kvd_status kvd_open_peer(kvd_cache local, const void* blob, size_t blob_len, kvd_peer* out) {
+  if (!local || !out) return fail(KVD_EINVAL, "null argument");
+  *out = nullptr;
+  Blob B;
+  kvd_status s = decode_blob(blob, blob_len, &B);
+  if (s != KVD_OK) return s;
+  Geom rg;
+  s = make_geom(&B.layout, &rg);
+  if (s != KVD_OK) return fail(KVD_EHANDLE, "blob layout invalid: %s", g_last_error.c_str());
+  // compatibility (row b): what must be equal
+  const kvd_layout& A = local->geom.layout;
+  const kvd_layout& R = rg.layout;
+  if (A.num_layers != R.num_layers || A.num_kv_heads != R.num_kv_heads ||
+      A.head_dim != R.head_dim || A.block_size != R.block_size ||
+      elem_size(A.dtype) != elem_size(R.dtype))
+    return fail(KVD_ELAYOUT,
+                "incompatible caches: layers %u/%u heads %u/%u head_dim %u/%u block %u/%u elem %u/%u",
+                R.num_layers, A.num_layers, R.num_kv_heads, A.num_kv_heads, R.head_dim, A.head_dim,
+                R.block_size, A.block_size, elem_size(R.dtype), elem_size(A.dtype));
+  if (R.stride[kL] != A.stride[kL] || R.stride[kH] != A.stride[kH] || R.stride[kD] != A.stride[kD])
+    return fail(KVD_ELAYOUT, "incompatible (L, H, D) order between prefill and decode caches");
+
+  std::unique_ptr<kvd_peer_s, void (*)(kvd_peer)> p(new (std::nothrow) kvd_peer_s(), peer_release);
+  if (!p) return fail(KVD_ENOMEM, "host allocation");
+  p->local = local;
+  p->remote = rg;
+  p->remote_device = B.device;
+  p->same_process = (B.pid == (int64_t)getpid() && B.nonce == process_nonce());
+
+  DeviceGuard dg(local->device);
+  if (!dg.ok) return fail(KVD_ECUDA, "cannot select device %d", local->device);
+  std::vector<uint64_t> alloc_va(B.allocs.size());
+  if (p->same_process) {
+    for (size_t i = 0; i < B.allocs.size(); ++i) alloc_va[i] = B.allocs[i].base;
+    if (B.device != local->device) {
+      int can = 0;
+      KVD_CUDA(cudaDeviceCanAccessPeer(&can, local->device, B.device));
+      if (!can) return fail(KVD_EHANDLE, "device %d cannot access peer %d", local->device, B.device);
+      cudaError_t e = cudaDeviceEnablePeerAccess(B.device, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+      else if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+    }
+  } else {
+    for (size_t i = 0; i < B.allocs.size(); ++i) {
+      void* ptr = nullptr;
+      s = ipc_open(B.allocs[i].handle, local->device, &ptr);
+      if (s != KVD_OK) return s;
+      p->opened.push_back(B.allocs[i].handle);
+      alloc_va[i] = (uint64_t)(uintptr_t)ptr;
+    }
+  }
+  std::vector<uint64_t> src(B.layers.size());
+  for (size_t l = 0; l < B.layers.size(); ++l) {
+    const auto& bl = B.layers[l];
+    if (bl.offset + rg.g.layer_bytes > B.allocs[bl.alloc].size)
+      return fail(KVD_EHANDLE, "blob: layer %zu overruns its allocation", l);
+    src[l] = alloc_va[bl.alloc] + bl.offset;
+    if (src[l] % 16) return fail(KVD_ELAYOUT, "remote layer %zu not 16 B aligned", l);
+  }
+  p->src_bases = src;
+  KVD_CUDA(cudaMalloc(&p->d_src_bases, src.size() * sizeof(uint64_t)));
+  KVD_CUDA(cudaMemcpy(p->d_src_bases, src.data(), src.size() * sizeof(uint64_t),
+                      cudaMemcpyHostToDevice));
+  KVD_CUDA(cudaHostAlloc((void**)&p->flags, kSlots * sizeof(unsigned long long),
+                         cudaHostAllocMapped | cudaHostAllocPortable));
+  memset(p->flags, 0, kSlots * sizeof(unsigned long long));
+  KVD_CUDA(cudaHostGetDevicePointer((void**)&p->flags_dev, p->flags, 0));
+  KVD_CUDA(cudaMalloc(&p->counters, kSlots * sizeof(unsigned int)));
+  KVD_CUDA(cudaMemset(p->counters, 0, kSlots * sizeof(unsigned int)));
+  KVD_CUDA(cudaDeviceSynchronize());
+  p->slot_seq.assign(kSlots, 0);
+  p->slot_runs_dev.assign(kSlots, nullptr);
+  p->slot_runs_host.assign(kSlots, nullptr);
+  p->slot_runs_cap.assign(kSlots, 0);
+  KVD_CUDA(cudaDeviceGetAttribute(&p->sm_count, cudaDevAttrMultiProcessorCount, local->device));
+  *out = p.release();
+  return KVD_OK;
+}
+
+kvd_status kvd_close_peer(kvd_peer p) {
+  if (!p) return fail(KVD_EINVAL, "null peer");
+  {
+    std::lock_guard<std::mutex> lk(p->mu);
+    p->closed = true;
+  }
+  peer_release(p);
+  return KVD_OK;
+}
+
+kvd_status kvd_peer_set(kvd_peer p, int option, int64_t value) {
+  if (!p) return fail(KVD_EINVAL, "null peer");
+  std::lock_guard<std::mutex> lk(p->mu);
+  switch (option) {
+    case KVD_OPT_MAX_CTAS:
+      if (value < 0 || value > (1 << 20)) return fail(KVD_EINVAL, "max_ctas %lld", (long long)value);
+      p->max_ctas = (uint32_t)value;
+      return KVD_OK;
+    case KVD_OPT_TILE_BYTES:
+      if (value < 512 || value % 512 || value > (1 << 24))
+        return fail(KVD_EINVAL, "tile_bytes must be a multiple of 512 in [512, 16 MiB]");
+      p->tile_bytes = (uint32_t)value;
+      return KVD_OK;
+    case KVD_OPT_COALESCE:
+      p->coalesce = value ? 1 : 0;
+      return KVD_OK;
+    case KVD_OPT_VARIANT:
+      if (value < KVD_VARIANT_AUTO || value > KVD_VARIANT_CE)
+        return fail(KVD_EINVAL, "variant %lld", (long long)value);
+      p->variant = (int)value;
+      return KVD_OK;
+    case KVD_OPT_THREADS:
+      if (value < 128 || value > 1024 || value % 32)
+        return fail(KVD_EINVAL, "threads must be a multiple of 32 in [128, 1024]");
+      p->threads = (uint32_t)value;
+      return KVD_OK;
+  }
+  return fail(KVD_EINVAL, "unknown option %d", option);
+}
+
+// ===========================================================================
+// ABI: a3-a6 pull
+// ===========================================================================
+kvd_status kvd_pull(kvd_peer p, uint64_t request_id, const int32_t* src_ids,
+                    const int32_t* dst_ids, uint32_t n, void* stream_) {
+  if (!p) return fail(KVD_EINVAL, "null peer");
+  std::lock_guard<std::mutex> lk(p->mu);
+  if (p->closed) return fail(KVD_ESTATE, "peer closed");
+  if (p->inflight.count(request_id))
+    return fail(KVD_EBUSY, "request %llu already in flight", (unsigned long long)request_id);
+  const kvd_geometry& sg = p->remote.g;
+  const kvd_geometry& dg_ = p->local->geom.g;
+  // a3: validate + coalesce
+  kvd_status s = p->planner.plan(src_ids, dst_ids, n, p->remote.layout.num_blocks,
+                                 p->local->geom.layout.num_blocks, p->coalesce != 0, p->runs);
+  if (s != KVD_OK) return s;
+  const PairPlan pp = pair_plan(sg, dg_);
+  const uint32_t NL = p->local->geom.layout.num_layers;
+  kvd::PullArgs a{};
+  a.src = kvd::SideAddr{p->d_src_bases, 0, 0, sg.plane_stride_bytes, sg.block_stride_bytes};
+  a.dst = kvd::SideAddr{p->local->d_bases, 0, 0, dg_.plane_stride_bytes, dg_.block_stride_bytes};
+  if (n) {
+    s = tile_runs(p->runs, pp, NL, p->tile_bytes, p->runs4, a);
+    if (s != KVD_OK) return s;
+  }
+  // a6: completion slot
+  uint32_t slot = kSlots;
+  for (uint32_t k = 0; k < kSlots; ++k) {
+    const uint32_t c = (p->cursor + k) % kSlots;
+    if (p->slot_seq[c] == 0) { slot = c; break; }
+  }
+  if (slot == kSlots) return fail(KVD_EBUSY, "all %u completion slots in flight (poll them)", kSlots);
+  const uint64_t token = ++p->seq;
+  a.counter = p->counters + slot;
+  a.flag = p->flags_dev + slot;
+  a.token = token;
+
+  DeviceGuard dgd(p->local->device);
+  if (!dgd.ok) return fail(KVD_ECUDA, "cannot select device %d", p->local->device);
+  cudaStream_t stream = (cudaStream_t)stream_;
+  kvd_pull_info info{};
+  info.request_id = request_id;
+  info.blocks = n;
+  info.runs = (uint32_t)p->runs.size();
+  info.bytes = (uint64_t)n * NL * 2 * sg.span_bytes;
+  int variant = p->variant == KVD_VARIANT_AUTO ? KVD_VARIANT_LSU : p->variant;
+  cudaError_t e = cudaSuccess;
+  if (n == 0) {
+    e = kvd::launch_flag_only(a.flag, token, stream);
+    info.launches = 1;
+    info.ctas = 1;
+  } else if (variant == KVD_VARIANT_CE) {
+    // copy-engine comparator: one cudaMemcpyAsync per contiguous segment
+    const std::vector<uint64_t>& src_b = p->src_bases;
+    uint32_t launches = 0;
+    for (uint32_t l = 0; l < NL && e == cudaSuccess; ++l)
+      for (uint32_t pl = 0; pl < pp.planes && e == cudaSuccess; ++pl)
+        for (const kvd_run& r : p->runs) {
+          const uint32_t nb = pp.contiguous ? 1 : r.len;
+          const uint64_t bytes = pp.contiguous ? (uint64_t)r.len * pp.unit : pp.unit;
+          for (uint32_t j = 0; j < nb && e == cudaSuccess; ++j) {
+            const uint64_t so = src_b[l] + pl * sg.plane_stride_bytes + (uint64_t)(r.src_start + j) * sg.block_stride_bytes;
+            const uint64_t d0 = p->local->bases[l] + pl * dg_.plane_stride_bytes + (uint64_t)(r.dst_start + j) * dg_.block_stride_bytes;
+            e = cudaMemcpyAsync((void*)(uintptr_t)d0, (const void*)(uintptr_t)so, bytes,
+                                cudaMemcpyDeviceToDevice, stream);
+            ++launches;
+          }
+        }
+    if (e == cudaSuccess) e = kvd::launch_flag_only(a.flag, token, stream);
+    info.launches = launches + 1;
+    info.segments = launches;
+  } else {
+    if (variant == KVD_VARIANT_LSU32 && !aligned32(a, p->src_bases, p->local->bases))
+      variant = KVD_VARIANT_LSU;
+    // big run tables go through a per-slot device buffer
+    if (a.nruns > kvd::max_param_runs()) {
+      if (p->slot_runs_cap[slot] < a.nruns) {
+        if (p->slot_runs_dev[slot]) cudaFree(p->slot_runs_dev[slot]);
+        if (p->slot_runs_host[slot]) cudaFreeHost(p->slot_runs_host[slot]);
+        p->slot_runs_dev[slot] = nullptr;
+        p->slot_runs_host[slot] = nullptr;
+        p->slot_runs_cap[slot] = 0;
+        KVD_CUDA(cudaMalloc(&p->slot_runs_dev[slot], a.nruns * sizeof(int4)));
+        KVD_CUDA(cudaMallocHost(&p->slot_runs_host[slot], a.nruns * sizeof(int4)));
+        p->slot_runs_cap[slot] = a.nruns;
+      }
+      memcpy(p->slot_runs_host[slot], p->runs4.data(), a.nruns * sizeof(int4));
+      KVD_CUDA(cudaMemcpyAsync(p->slot_runs_dev[slot], p->slot_runs_host[slot],
+                               a.nruns * sizeof(int4), cudaMemcpyHostToDevice, stream));
+      a.runs_dev = p->slot_runs_dev[slot];
+      info.launches = 1;   // the H2D copy (not a kernel)
+    }
+    uint32_t max_ctas = p->max_ctas;
+    if (!max_ctas) {
+      const int per_sm = kvd::pull_ctas_per_sm(variant, p->threads, a.nruns);
+      max_ctas = (uint32_t)(p->sm_count * per_sm);
+    }
+    const uint32_t ctas = grid_for(a.total_tiles, p->threads, max_ctas);
+    e = kvd::launch_pull(a, p->runs4.data(), variant, ctas, p->threads, stream);
+    info.launches += 1;
+    info.ctas = ctas;
+    info.threads = p->threads;
+    info.tiles = a.total_tiles;
+    info.segments = (uint64_t)NL * pp.planes * (pp.contiguous ? p->runs.size() : n);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "pull launch");
+  info.variant = (uint32_t)variant;
+  p->slot_seq[slot] = token;
+  p->cursor = (slot + 1) % kSlots;
+  p->inflight[request_id] = std::make_pair(slot, token);
+  p->last = info;
+  return KVD_OK;
+}
+
+kvd_status kvd_poll_done(kvd_peer p, uint64_t request_id, int* done) {
+  if (!p || !done) return fail(KVD_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lk(p->mu);
+  auto it = p->inflight.find(request_id);
+  if (it == p->inflight.end())
+    return fail(KVD_EINVAL, "request %llu is not in flight", (unsigned long long)request_id);
+  const uint32_t slot = it->second.first;
+  const uint64_t token = it->second.second;
+  const uint64_t v = __atomic_load_n(&p->flags[slot], __ATOMIC_ACQUIRE);
+  if (v == token) {
+    *done = 1;
+    p->slot_seq[slot] = 0;
+    p->inflight.erase(it);
+  } else {
+    *done = 0;
+  }
+  return KVD_OK;
+}
+
+kvd_status kvd_wait_done(kvd_peer p, uint64_t request_id, int64_t timeout_us) {
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    int done = 0;
+    kvd_status s = kvd_poll_done(p, request_id, &done);
+    if (s != KVD_OK) return s;
+    if (done) return KVD_OK;
+    if (timeout_us >= 0 &&
+        std::chrono::duration_cast<std::chrono::microseconds>(std::chrono::steady_clock::now() - t0)
+                .count() > timeout_us)
+      return fail(KVD_EBUSY, "request %llu not done after %lld us", (unsigned long long)request_id,
+                  (long long)timeout_us);
+  }
+}
+
+kvd_status kvd_last_pull_info(kvd_peer p, kvd_pull_info* out) {
+  if (!p || !out) return fail(KVD_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lk(p->mu);
+  *out = p->last;
+  return KVD_OK;
+}
+
+// ===========================================================================
+// ABI: baseline gather / scatter (fig:diff(a) steps 2 and 4)
+// ===========================================================================
+static kvd_status gather_scatter(kvd_cache c, const int32_t* ids, uint32_t n, uint64_t staging,
+                                 void* stream_, bool gather) {
+  if (!c) return fail(KVD_EINVAL, "null cache");
+  if (n && (!ids || !staging)) return fail(KVD_EINVAL, "null argument");
+  if (staging % 16) return fail(KVD_ELAYOUT, "staging buffer not 16 B aligned");
+  if (!n) return KVD_OK;
+  std::lock_guard<std::mutex> lk(c->mu);
+  const kvd_geometry& g = c->geom.g;
+  const uint32_t NL = c->geom.layout.num_layers;
+  if (c->iota.size() < n) {
+    c->iota.resize(n);
+    for (uint32_t i = 0; i < n; ++i) c->iota[i] = (int32_t)i;
+  }
+  kvd_status s = gather ? c->planner.plan(ids, c->iota.data(), n, c->geom.layout.num_blocks, n, true, c->runs)
+                        : c->planner.plan(c->iota.data(), ids, n, n, c->geom.layout.num_blocks, true, c->runs);
+  if (s != KVD_OK) return s;
+  kvd_geometry sg{};
+  sg.span_bytes = g.span_bytes;
+  sg.block_stride_bytes = (int64_t)g.span_bytes;
+  sg.plane_stride_bytes = (int64_t)(n * g.span_bytes);
+  sg.kv_adjacent = 0;
+  const kvd::SideAddr cache_side{c->d_bases, 0, 0, g.plane_stride_bytes, g.block_stride_bytes};
+  const kvd::SideAddr stage_side{nullptr, staging, 2ull * n * g.span_bytes, sg.plane_stride_bytes,
+                                 sg.block_stride_bytes};
+  kvd::PullArgs a{};
+  a.src = gather ? cache_side : stage_side;
+  a.dst = gather ? stage_side : cache_side;
+  PairPlan pp = pair_plan(gather ? g : sg, gather ? sg : g);
+  s = tile_runs(c->runs, pp, NL, 16384, c->runs4, a);
+  if (s != KVD_OK) return s;
+  a.counter = nullptr;
+  a.flag = nullptr;
+  DeviceGuard dgd(c->device);
+  if (!dgd.ok) return fail(KVD_ECUDA, "cannot select device %d", c->device);
+  if (a.nruns > kvd::max_param_runs())
+    return fail(KVD_ERANGE, "baseline gather/scatter supports at most %u runs", kvd::max_param_runs());
+  int dev_sms = 148;
+  cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
+  const uint32_t threads = 512;
+  const uint32_t ctas = grid_for(a.total_tiles, threads,
+                                 (uint32_t)(dev_sms * kvd::pull_ctas_per_sm(KVD_VARIANT_LSU, threads, a.nruns)));
+  cudaError_t e = kvd::launch_pull(a, c->runs4.data(), KVD_VARIANT_LSU, ctas, threads,
+                                   (cudaStream_t)stream_);
+  if (e != cudaSuccess) return cuda_fail(e, gather ? "gather launch" : "scatter launch");
+  return KVD_OK;
+}
+
+kvd_status kvd_gather(kvd_cache c, const int32_t* ids, uint32_t n, void* staging, void* stream) {
+  return gather_scatter(c, ids, n, (uint64_t)(uintptr_t)staging, stream, true);
+}
+
+kvd_status kvd_scatter(kvd_cache c, const int32_t* ids, uint32_t n, const void* staging,
+                       void* stream) {
+  return gather_scatter(c, ids, n, (uint64_t)(uintptr_t)staging, stream, false);
+}
+
+}  // extern "C"

@@ -1,0 +1,62 @@
+// kvd_internal.h -- interface between the host core (kvd_core.cpp) and the
+// sm_100a kernels (kvd_pull.cu).  Not part of the public ABI (include/kvd.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace kvd {
+
+// Where layer l of one side starts: table ? table[l] : base + l * step.
+// The peer's source side uses a device table of IPC-mapped prefill layer
+// bases; the baseline staging buffer uses the affine form.
+struct SideAddr {
+  const unsigned long long* table;  // device array [num_layers] or nullptr
+  unsigned long long base;
+  unsigned long long step;
+  long long plane_stride;           // bytes between the K and V sub-tensors of a block
+  long long block_stride;           // bytes between consecutive blocks
+};
+
+// Everything one pull launch needs except the run table.
+//
+// Work decomposition: the request is a set of
+// segments (layer l, plane p, run r).  Each segment is cut into "tiles" of at
+// most tile_bytes that never cross a segment; one WARP copies one tile.
+// runs[r] = {src_start, dst_start, len, tile_end} where tile_end is the
+// inclusive prefix sum of tiles over runs 0..r within one (layer, plane).
+struct PullArgs {
+  SideAddr src, dst;
+  unsigned long long unit_bytes;    // bytes of one (block, plane) unit: span, or 2*span when K,V adjacent on both sides
+  unsigned int num_layers;
+  unsigned int planes;              // 2, or 1 when the unit folds K and V
+  unsigned int tile_bytes;          // multiple of 512
+  unsigned int contiguous;          // 1: a run is one byte-contiguous segment on both sides
+  unsigned int tiles_per_unit;      // ceil(unit_bytes / tile_bytes) (non-contiguous runs)
+  unsigned int nruns;
+  unsigned int tiles_per_lp;        // tiles of one (layer, plane) = runs[nruns-1].w
+  unsigned int total_tiles;         // num_layers * planes * tiles_per_lp
+  unsigned int* counter;            // per-slot arrive counter (device, zero at launch)
+  unsigned long long* flag;         // per-slot completion word (pinned, host-mapped)
+  unsigned long long token;         // value stored to *flag when every byte has landed
+  const int4* runs_dev;             // run table in device memory when nruns > params capacity
+};
+
+enum Variant : int { kLsu16 = 1, kLsu32 = 2 };
+
+// Largest run table that travels inside the kernel parameters.
+unsigned int max_param_runs();
+
+// Launch one pull kernel.  runs_host must hold args.nruns entries when
+// args.nruns <= max_param_runs(); otherwise args.runs_dev is used.
+cudaError_t launch_pull(const PullArgs& args, const int4* runs_host, int variant,
+                        unsigned int ctas, unsigned int threads, cudaStream_t stream);
+
+// Completion with no bytes (n = 0, or after copy-engine copies).
+cudaError_t launch_flag_only(unsigned long long* flag, unsigned long long token,
+                             cudaStream_t stream);
+
+// Resident CTAs per SM of the pull kernel for the given threads per CTA.
+int pull_ctas_per_sm(int variant, unsigned int threads, unsigned int nruns);
+
+}  // namespace kvd

@@ -1,0 +1,216 @@
+// kvd_pull.cu -- the sm_100a pull kernel and its
+// completion epilogue (row a6).
+//
+// PAPER.md §4.3: in pull mode the decode worker "reads the blocks
+// from the prefill worker" and "performs KV cache reads for all layers in a
+// single shot".  Here the reads are one-sided SM loads from the prefill
+// GPU's HBM, mapped into this process with CUDA IPC, over NVLink 5 /
+// NVSwitch; the writes are local HBM stores into the decode cache's blocks.
+// One launch covers every layer, both K and V, and every coalesced run
+// (P:L377-378); the last CTA to finish raises the request's completion word
+// ("The completion transaction sends the request ID"), so the host
+// never synchronises per block.
+//
+// The copy is a bit copy through integer vector registers only (no float
+// type ever touches the data), so NaN payloads, -0 and subnormals survive.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "kvd_internal.h"
+
+namespace kvd {
+namespace {
+
+// Param-resident run tables.  CUDA 12.1+ allows 32764 bytes of kernel
+// parameters; PullArgs is ~160 B, so 2016 int4 runs fit.
+constexpr int kRunsSmall = 64;
+constexpr int kRunsMid = 512;
+constexpr int kRunsLarge = 2016;
+
+template <int MAXR>
+struct PullParams {
+  PullArgs a;
+  int4 runs[MAXR > 0 ? MAXR : 1];
+};
+
+// ---------------------------------------------------------------------------
+// vector load/store: peer loads go through the non-coherent path without
+// allocating in L1 (each byte is read exactly once); stores are plain.
+// ---------------------------------------------------------------------------
+struct alignas(16) V16 { uint32_t x, y, z, w; };
+struct alignas(32) V32 { uint32_t v[8]; };
+
+__device__ __forceinline__ V16 ld_peer(const V16* p) {
+  V16 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_local(V16* p, const V16& v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};"
+               :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+__device__ __forceinline__ V32 ld_peer(const V32* p) {
+  V32 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r.v[0]), "=r"(r.v[1]), "=r"(r.v[2]), "=r"(r.v[3]),
+                 "=r"(r.v[4]), "=r"(r.v[5]), "=r"(r.v[6]), "=r"(r.v[7]) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_local(V32* p, const V32& v) {
+  asm volatile("st.global.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+               :: "l"(p), "r"(v.v[0]), "r"(v.v[1]), "r"(v.v[2]), "r"(v.v[3]),
+                  "r"(v.v[4]), "r"(v.v[5]), "r"(v.v[6]), "r"(v.v[7]) : "memory");
+}
+
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+}
+
+// One warp copies `bytes` (multiple of sizeof(V)) from src to dst.  All U
+// loads of a batch are issued before any store so each lane keeps U
+// independent NVLink reads in flight (Little's law).
+template <typename V, int U>
+__device__ __forceinline__ void warp_copy(char* __restrict__ dst, const char* __restrict__ src,
+                                          unsigned int bytes, unsigned int lane) {
+  const V* s = reinterpret_cast<const V*>(src);
+  V* d = reinterpret_cast<V*>(dst);
+  const unsigned int nv = bytes / sizeof(V);
+  for (unsigned int i = lane; i < nv; i += 32 * U) {
+    V v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (i + u * 32 < nv) v[u] = ld_peer(s + i + u * 32);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (i + u * 32 < nv) st_local(d + i + u * 32, v[u]);
+  }
+}
+
+__device__ __forceinline__ unsigned long long layer_base(const SideAddr& s, unsigned int l) {
+  return s.table ? s.table[l] : s.base + (unsigned long long)l * s.step;
+}
+
+template <int MAXR, typename V, int U>
+__global__ void __launch_bounds__(1024)
+pull_kernel(const __grid_constant__ PullParams<MAXR> P) {
+  const PullArgs& a = P.a;
+  const int4* runs = (MAXR > 0) ? P.runs : a.runs_dev;
+  const unsigned int lane = threadIdx.x & 31u;
+  const unsigned int warps_per_cta = blockDim.x >> 5;
+  const unsigned int nwarps = gridDim.x * warps_per_cta;
+
+  for (unsigned int t = blockIdx.x * warps_per_cta + (threadIdx.x >> 5); t < a.total_tiles;
+       t += nwarps) {
+    // tile -> (layer, plane, run, offset); all warp-uniform
+    const unsigned int lp = t / a.tiles_per_lp;
+    const unsigned int k = t - lp * a.tiles_per_lp;
+    const unsigned int l = (a.planes == 2) ? (lp >> 1) : lp;
+    const unsigned int p = (a.planes == 2) ? (lp & 1u) : 0u;
+    int lo = 0, hi = (int)a.nruns - 1;                 // first run with tile_end > k
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if ((unsigned int)runs[mid].w > k) hi = mid; else lo = mid + 1;
+    }
+    const int4 run = runs[lo];
+    const unsigned int kr = k - (lo ? (unsigned int)runs[lo - 1].w : 0u);
+
+    unsigned long long src_off, dst_off, off, avail;
+    if (a.contiguous) {
+      off = (unsigned long long)kr * a.tile_bytes;
+      avail = (unsigned long long)(unsigned int)run.z * a.unit_bytes - off;
+      src_off = (unsigned long long)run.x * a.src.block_stride + off;
+      dst_off = (unsigned long long)run.y * a.dst.block_stride + off;
+    } else {
+      const unsigned int j = kr / a.tiles_per_unit;
+      const unsigned int kk = kr - j * a.tiles_per_unit;
+      off = (unsigned long long)kk * a.tile_bytes;
+      avail = a.unit_bytes - off;
+      src_off = (unsigned long long)(run.x + (int)j) * a.src.block_stride + off;
+      dst_off = (unsigned long long)(run.y + (int)j) * a.dst.block_stride + off;
+    }
+    const unsigned int bytes = avail < a.tile_bytes ? (unsigned int)avail : a.tile_bytes;
+    const char* src = reinterpret_cast<const char*>(
+        layer_base(a.src, l) + (unsigned long long)p * a.src.plane_stride + src_off);
+    char* dst = reinterpret_cast<char*>(
+        layer_base(a.dst, l) + (unsigned long long)p * a.dst.plane_stride + dst_off);
+    warp_copy<V, U>(dst, src, bytes, lane);
+  }
+
+  // Completion (row a6): every thread orders its stores at gpu scope, the
+  // CTA arrives once; the last CTA resets the slot counter and publishes the
+  // token with a system-scope release so a host acquire load of the flag
+  // implies every byte of the request is visible.
+  if (a.counter == nullptr) return;   // baseline gather/scatter: stream order only
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int prev = atomicAdd(a.counter, 1u);
+    if (prev == gridDim.x - 1) {
+      *a.counter = 0u;
+      __threadfence_system();
+      st_release_sys(a.flag, a.token);
+    }
+  }
+}
+
+__global__ void flag_kernel(unsigned long long* flag, unsigned long long token) {
+  __threadfence_system();
+  st_release_sys(flag, token);
+}
+
+template <int MAXR, typename V, int U>
+cudaError_t launch_t(const PullArgs& args, const int4* runs_host, unsigned int ctas,
+                     unsigned int threads, cudaStream_t stream) {
+  PullParams<MAXR> P;
+  P.a = args;
+  if (MAXR > 0)
+    for (unsigned int r = 0; r < args.nruns; ++r) P.runs[r] = runs_host[r];
+  pull_kernel<MAXR, V, U><<<ctas, threads, 0, stream>>>(P);
+  return cudaGetLastError();
+}
+
+template <typename V, int U>
+cudaError_t launch_v(const PullArgs& args, const int4* runs_host, unsigned int ctas,
+                     unsigned int threads, cudaStream_t stream) {
+  if (args.nruns <= (unsigned)kRunsSmall)
+    return launch_t<kRunsSmall, V, U>(args, runs_host, ctas, threads, stream);
+  if (args.nruns <= (unsigned)kRunsMid)
+    return launch_t<kRunsMid, V, U>(args, runs_host, ctas, threads, stream);
+  if (args.nruns <= (unsigned)kRunsLarge)
+    return launch_t<kRunsLarge, V, U>(args, runs_host, ctas, threads, stream);
+  return launch_t<0, V, U>(args, runs_host, ctas, threads, stream);
+}
+
+template <int MAXR, typename V, int U>
+int occ(unsigned int threads) {
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, pull_kernel<MAXR, V, U>, (int)threads,
+                                                    0) != cudaSuccess)
+    return 1;
+  return n > 0 ? n : 1;
+}
+
+}  // namespace
+
+unsigned int max_param_runs() { return (unsigned int)kRunsLarge; }
+
+cudaError_t launch_pull(const PullArgs& args, const int4* runs_host, int variant,
+                        unsigned int ctas, unsigned int threads, cudaStream_t stream) {
+  if (variant == kLsu32) return launch_v<V32, 4>(args, runs_host, ctas, threads, stream);
+  return launch_v<V16, 8>(args, runs_host, ctas, threads, stream);
+}
+
+cudaError_t launch_flag_only(unsigned long long* flag, unsigned long long token,
+                             cudaStream_t stream) {
+  flag_kernel<<<1, 1, 0, stream>>>(flag, token);
+  return cudaGetLastError();
+}
+
+int pull_ctas_per_sm(int variant, unsigned int threads, unsigned int nruns) {
+  const bool big = nruns > (unsigned)kRunsLarge;
+  if (variant == kLsu32) return big ? occ<0, V32, 4>(threads) : occ<kRunsSmall, V32, 4>(threads);
+  return big ? occ<0, V16, 8>(threads) : occ<kRunsSmall, V16, 8>(threads);
+}
+
+}  // namespace kvd

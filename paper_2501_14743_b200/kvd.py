@@ -1,0 +1,246 @@
+"""Thin ctypes binding of the C ABI in include/kvd.h (argument marshalling
+only: every step of the pull runs in libkvd.so -- host core + sm_100a
+kernels).  Function names are the C names; a negative kvd_status raises
+``KvdError`` carrying the status and kvd_last_error().
+
+There is no CPU fallback: if libkvd.so is missing the import fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libkvd.so")
+
+OK, EINVAL, ERANGE, ELAYOUT, EHANDLE, ECUDA, ENOMEM, EBUSY, ESTATE = 0, -1, -2, -3, -4, -5, -6, -7, -8
+FP16, BF16, FP8, FP32 = 0, 1, 2, 3
+VARIANT_AUTO, VARIANT_LSU, VARIANT_LSU32, VARIANT_CE = 0, 1, 2, 3
+OPT_MAX_CTAS, OPT_TILE_BYTES, OPT_COALESCE, OPT_VARIANT, OPT_THREADS = 0, 1, 2, 3, 4
+
+EXPORTED = (
+    "kvd_layout_geometry", "kvd_plan", "kvd_blob_info", "kvd_register_cache",
+    "kvd_unregister_cache", "kvd_export_handle", "kvd_open_peer", "kvd_close_peer",
+    "kvd_peer_set", "kvd_pull", "kvd_poll_done", "kvd_wait_done", "kvd_last_pull_info",
+    "kvd_gather", "kvd_scatter", "kvd_strerror", "kvd_last_error", "kvd_abi_version",
+)
+
+
+class kvd_layout(ctypes.Structure):
+    _fields_ = [("num_layers", ctypes.c_uint32), ("num_kv_heads", ctypes.c_uint32),
+                ("head_dim", ctypes.c_uint32), ("block_size", ctypes.c_uint32),
+                ("num_blocks", ctypes.c_uint32), ("dtype", ctypes.c_uint32),
+                ("stride", ctypes.c_int64 * 5)]
+
+
+class kvd_geometry(ctypes.Structure):
+    _fields_ = [("span_bytes", ctypes.c_uint64), ("block_stride_bytes", ctypes.c_int64),
+                ("plane_stride_bytes", ctypes.c_int64), ("layer_bytes", ctypes.c_uint64),
+                ("elem_bytes", ctypes.c_uint32), ("kv_adjacent", ctypes.c_uint32)]
+
+
+class kvd_run(ctypes.Structure):
+    _fields_ = [("src_start", ctypes.c_int32), ("dst_start", ctypes.c_int32),
+                ("len", ctypes.c_uint32)]
+
+
+class kvd_pull_info(ctypes.Structure):
+    _fields_ = [("request_id", ctypes.c_uint64), ("bytes", ctypes.c_uint64),
+                ("blocks", ctypes.c_uint32), ("runs", ctypes.c_uint32),
+                ("segments", ctypes.c_uint64), ("tiles", ctypes.c_uint64),
+                ("ctas", ctypes.c_uint32), ("threads", ctypes.c_uint32),
+                ("variant", ctypes.c_uint32), ("launches", ctypes.c_uint32)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class KvdError(RuntimeError):
+    def __init__(self, status: int, where: str, detail: str):
+        super().__init__(f"{where}: status {status} ({detail})")
+        self.status = status
+
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+        "(there is no CPU fallback)")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+_p = ctypes.c_void_p
+_u32, _u64, _i32, _i64 = ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int32, ctypes.c_int64
+_pi32 = ctypes.POINTER(ctypes.c_int32)
+
+_SIGS = {
+    "kvd_layout_geometry": [ctypes.POINTER(kvd_layout), ctypes.POINTER(kvd_geometry)],
+    "kvd_plan": [_pi32, _pi32, _u32, _u32, _u32, ctypes.c_int, ctypes.POINTER(kvd_run), _u32,
+                 ctypes.POINTER(_u32)],
+    "kvd_blob_info": [_p, ctypes.c_size_t, ctypes.POINTER(kvd_layout), ctypes.POINTER(_i32),
+                      ctypes.POINTER(_i64), ctypes.POINTER(_u32)],
+    "kvd_register_cache": [ctypes.c_int, ctypes.POINTER(kvd_layout), ctypes.POINTER(_p),
+                           ctypes.POINTER(_p)],
+    "kvd_unregister_cache": [_p],
+    "kvd_export_handle": [_p, _p, ctypes.POINTER(ctypes.c_size_t)],
+    "kvd_open_peer": [_p, _p, ctypes.c_size_t, ctypes.POINTER(_p)],
+    "kvd_close_peer": [_p],
+    "kvd_peer_set": [_p, ctypes.c_int, _i64],
+    "kvd_pull": [_p, _u64, _pi32, _pi32, _u32, _p],
+    "kvd_poll_done": [_p, _u64, ctypes.POINTER(ctypes.c_int)],
+    "kvd_wait_done": [_p, _u64, _i64],
+    "kvd_last_pull_info": [_p, ctypes.POINTER(kvd_pull_info)],
+    "kvd_gather": [_p, _pi32, _u32, _p, _p],
+    "kvd_scatter": [_p, _pi32, _u32, _p, _p],
+}
+for _name, _args in _SIGS.items():
+    _fn = getattr(_lib, _name)
+    _fn.argtypes = _args
+    _fn.restype = ctypes.c_int
+_lib.kvd_strerror.argtypes = [ctypes.c_int]
+_lib.kvd_strerror.restype = ctypes.c_char_p
+_lib.kvd_last_error.argtypes = []
+_lib.kvd_last_error.restype = ctypes.c_char_p
+_lib.kvd_abi_version.argtypes = []
+_lib.kvd_abi_version.restype = ctypes.c_int
+
+
+def _check(status: int, where: str) -> int:
+    if status < 0:
+        raise KvdError(status, where, _lib.kvd_last_error().decode(errors="replace"))
+    return status
+
+
+def _ids(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int32).reshape(-1))
+
+
+def _ptr_i32(a: np.ndarray):
+    return a.ctypes.data_as(_pi32) if a.size else None
+
+
+def make_layout(num_layers, num_kv_heads, head_dim, block_size, num_blocks, dtype=FP16,
+                stride=(0, 0, 0, 0, 0)) -> kvd_layout:
+    L = kvd_layout(num_layers, num_kv_heads, head_dim, block_size, num_blocks, dtype)
+    for k in range(5):
+        L.stride[k] = int(stride[k])
+    return L
+
+
+# ----------------------------------------------------------------------------
+# the ABI, one function per C entry point
+# ----------------------------------------------------------------------------
+
+def kvd_abi_version() -> int:
+    return _lib.kvd_abi_version()
+
+
+def kvd_strerror(status: int) -> str:
+    return _lib.kvd_strerror(status).decode()
+
+
+def kvd_last_error() -> str:
+    return _lib.kvd_last_error().decode(errors="replace")
+
+
+def kvd_layout_geometry(layout: kvd_layout) -> kvd_geometry:
+    g = kvd_geometry()
+    _check(_lib.kvd_layout_geometry(ctypes.byref(layout), ctypes.byref(g)), "kvd_layout_geometry")
+    return g
+
+
+def kvd_plan(src_ids, dst_ids, src_num_blocks: int, dst_num_blocks: int,
+             coalesce: bool = True) -> np.ndarray:
+    """Returns an (m, 3) int64 array of runs (src_start, dst_start, len)."""
+    s, d = _ids(src_ids), _ids(dst_ids)
+    if s.size != d.size:
+        raise ValueError("src_ids and dst_ids differ in length")
+    cap = max(1, s.size)
+    runs = (kvd_run * cap)()
+    m = _u32(0)
+    _check(_lib.kvd_plan(_ptr_i32(s), _ptr_i32(d), s.size, src_num_blocks, dst_num_blocks,
+                         1 if coalesce else 0, runs, cap, ctypes.byref(m)), "kvd_plan")
+    return np.array([(runs[i].src_start, runs[i].dst_start, runs[i].len) for i in range(m.value)],
+                    dtype=np.int64).reshape(-1, 3)
+
+
+def kvd_blob_info(blob: bytes):
+    L = kvd_layout()
+    dev, pid, na = _i32(0), _i64(0), _u32(0)
+    _check(_lib.kvd_blob_info(blob, len(blob), ctypes.byref(L), ctypes.byref(dev),
+                              ctypes.byref(pid), ctypes.byref(na)), "kvd_blob_info")
+    return L, dev.value, pid.value, na.value
+
+
+def kvd_register_cache(device: int, layout: kvd_layout, layer_base_dev: Sequence[int]) -> int:
+    arr = (_p * len(layer_base_dev))(*[int(b) for b in layer_base_dev])
+    h = _p()
+    _check(_lib.kvd_register_cache(int(device), ctypes.byref(layout), arr, ctypes.byref(h)),
+           "kvd_register_cache")
+    return h.value
+
+
+def kvd_unregister_cache(cache: int) -> None:
+    _check(_lib.kvd_unregister_cache(cache), "kvd_unregister_cache")
+
+
+def kvd_export_handle(cache: int) -> bytes:
+    n = ctypes.c_size_t(0)
+    st = _lib.kvd_export_handle(cache, None, ctypes.byref(n))
+    if st not in (OK, ENOMEM):
+        _check(st, "kvd_export_handle")
+    buf = ctypes.create_string_buffer(n.value)
+    _check(_lib.kvd_export_handle(cache, buf, ctypes.byref(n)), "kvd_export_handle")
+    return buf.raw[:n.value]
+
+
+def kvd_open_peer(local_dst: int, blob: bytes) -> int:
+    h = _p()
+    _check(_lib.kvd_open_peer(local_dst, blob, len(blob), ctypes.byref(h)), "kvd_open_peer")
+    return h.value
+
+
+def kvd_close_peer(peer: int) -> None:
+    _check(_lib.kvd_close_peer(peer), "kvd_close_peer")
+
+
+def kvd_peer_set(peer: int, option: int, value: int) -> None:
+    _check(_lib.kvd_peer_set(peer, option, int(value)), "kvd_peer_set")
+
+
+def kvd_pull(peer: int, request_id: int, src_ids, dst_ids, stream: Optional[int] = None) -> None:
+    """`stream`: a cudaStream_t as int (e.g. torch.cuda.current_stream().cuda_stream)."""
+    s, d = _ids(src_ids), _ids(dst_ids)
+    if s.size != d.size:
+        raise ValueError("src_ids and dst_ids differ in length")
+    _check(_lib.kvd_pull(peer, request_id, _ptr_i32(s), _ptr_i32(d), s.size, stream or None),
+           "kvd_pull")
+
+
+def kvd_poll_done(peer: int, request_id: int) -> bool:
+    done = ctypes.c_int(0)
+    _check(_lib.kvd_poll_done(peer, request_id, ctypes.byref(done)), "kvd_poll_done")
+    return bool(done.value)
+
+
+def kvd_wait_done(peer: int, request_id: int, timeout_us: int = 10_000_000) -> None:
+    _check(_lib.kvd_wait_done(peer, request_id, timeout_us), "kvd_wait_done")
+
+
+def kvd_last_pull_info(peer: int) -> kvd_pull_info:
+    info = kvd_pull_info()
+    _check(_lib.kvd_last_pull_info(peer, ctypes.byref(info)), "kvd_last_pull_info")
+    return info
+
+
+def kvd_gather(cache: int, ids, staging_dev: int, stream: Optional[int] = None) -> None:
+    a = _ids(ids)
+    _check(_lib.kvd_gather(cache, _ptr_i32(a), a.size, staging_dev, stream or None), "kvd_gather")
+
+
+def kvd_scatter(cache: int, ids, staging_dev: int, stream: Optional[int] = None) -> None:
+    a = _ids(ids)
+    _check(_lib.kvd_scatter(cache, _ptr_i32(a), a.size, staging_dev, stream or None),
+           "kvd_scatter")

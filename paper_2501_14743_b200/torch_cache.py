@@ -1,0 +1,102 @@
+"""Paged KV caches as torch device memory, registered with libkvd.
+
+torch is only the allocator and stream provider here: a ``PagedCache`` owns
+one uint8 tensor per layer (vLLM keeps one tensor per layer) -- or one
+tensor sliced into layers -- sized by the library's own geometry
+(kvd_layout_geometry), and registers the layer bases with
+kvd_register_cache.  Every byte of a pull is moved by libkvd's kernel.
+"""
+from __future__ import annotations
+
+from typing import List, Optional, Sequence
+
+import torch
+
+from . import kvd
+
+
+class PagedCache:
+    def __init__(self, num_layers: int, num_kv_heads: int, head_dim: int, block_size: int,
+                 num_blocks: int, dtype: int = kvd.FP16, stride: Sequence[int] = (0,) * 5,
+                 device: int = 0, single_allocation: bool = False, pad_bytes: int = 0):
+        self.layout = kvd.make_layout(num_layers, num_kv_heads, head_dim, block_size, num_blocks,
+                                      dtype, stride)
+        self.geom = kvd.kvd_layout_geometry(self.layout)
+        self.device = int(device)
+        self.layer_bytes = int(self.geom.layer_bytes)
+        # round each layer to 512 B so every base stays 32 B aligned
+        self.layer_pitch = (self.layer_bytes + pad_bytes + 511) // 512 * 512
+        dev = torch.device("cuda", self.device)
+        if single_allocation:
+            self._storage = torch.empty(self.layer_pitch * num_layers, dtype=torch.uint8,
+                                        device=dev)
+            self.layers: List[torch.Tensor] = [
+                self._storage[l * self.layer_pitch:l * self.layer_pitch + self.layer_bytes]
+                for l in range(num_layers)]
+        else:
+            self._storage = None
+            self.layers = [torch.empty(self.layer_bytes, dtype=torch.uint8, device=dev)
+                           for _ in range(num_layers)]
+        self.handle: Optional[int] = kvd.kvd_register_cache(
+            self.device, self.layout, [t.data_ptr() for t in self.layers])
+
+    @property
+    def num_blocks(self) -> int:
+        return self.layout.num_blocks
+
+    @property
+    def span_bytes(self) -> int:
+        return int(self.geom.span_bytes)
+
+    def export(self) -> bytes:
+        return kvd.kvd_export_handle(self.handle)
+
+    def open_peer(self, blob: bytes) -> "Peer":
+        return Peer(self, kvd.kvd_open_peer(self.handle, blob))
+
+    def close(self) -> None:
+        if self.handle:
+            kvd.kvd_unregister_cache(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Peer:
+    """Decode-side binding of a prefill cache (kvd_peer)."""
+
+    def __init__(self, local: PagedCache, handle: int):
+        self.local = local
+        self.handle: Optional[int] = handle
+
+    def set(self, option: int, value: int) -> "Peer":
+        kvd.kvd_peer_set(self.handle, option, value)
+        return self
+
+    def pull(self, request_id: int, src_ids, dst_ids, stream: Optional[torch.cuda.Stream] = None):
+        s = stream if stream is not None else torch.cuda.current_stream(self.local.device)
+        kvd.kvd_pull(self.handle, request_id, src_ids, dst_ids, s.cuda_stream)
+
+    def poll(self, request_id: int) -> bool:
+        return kvd.kvd_poll_done(self.handle, request_id)
+
+    def wait(self, request_id: int, timeout_us: int = 30_000_000) -> None:
+        kvd.kvd_wait_done(self.handle, request_id, timeout_us)
+
+    def info(self) -> dict:
+        return kvd.kvd_last_pull_info(self.handle).as_dict()
+
+    def close(self) -> None:
+        if self.handle:
+            kvd.kvd_close_peer(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,348 @@
+"""GPU parity of the pull path (C ABI -> sm_100a kernel) against the CPU oracle.
+
+Every test compares the decode cache after kvd_pull, byte for byte, with the
+oracle's result on host copies of the same seeded inputs (SURVEY.md §8 row c
+P3: unique result, bit-exact).  On a one-GPU box the prefill and decode
+caches share the GPU (loopback); tests marked gpu2 use two GPUs.
+"""
+import numpy as np
+import pytest
+import torch
+
+import kvdgen
+from gpu_helpers import (assert_layers_equal, make_pair, next_request_id, pull_and_wait)
+from paper_2501_14743_b200 import kvd
+
+pytestmark = pytest.mark.gpu
+
+C1 = kvdgen.C1
+N_C1 = kvdgen.blocks_for(kvdgen.C1_TOKENS, C1.block_size)
+
+
+def _tables(kind, n, nb_s, nb_d, seed):
+    if kind == "contiguous":
+        return kvdgen.contiguous_table(n, 0, nb_d - n)
+    if kind == "fragmented":
+        return kvdgen.fragmented_table(n, nb_s, nb_d, seed)
+    if kind == "random":
+        return kvdgen.random_table(n, nb_s, nb_d, seed)
+    if kind == "reversed":
+        s, d = kvdgen.contiguous_table(n, 0, 0)
+        return s, d[::-1].copy()
+    raise ValueError(kind)
+
+
+@pytest.mark.parametrize("kind", ["contiguous", "fragmented", "random", "reversed"])
+def test_c1_bit_exact(kind):
+    pair = make_pair(C1, C1, seed=1)
+    try:
+        src, dst = _tables(kind, N_C1, C1.num_blocks, C1.num_blocks, seed=0)
+        info = pull_and_wait(pair, src, dst)
+        assert info["blocks"] == N_C1 and info["bytes"] == N_C1 * C1.num_layers * 2 * 4096
+        assert_layers_equal(pair.download_dst(), pair.expected(src, dst))
+        # I3: the source cache is unchanged
+        torch.cuda.synchronize()
+        for l, t in enumerate(pair.src.layers):
+            assert np.array_equal(t.cpu().numpy(), pair.src_host[l])
+    finally:
+        pair.close()
+
+
+SUB = 16 * 2 * 64   # C1 sub-tensor elements
+
+
+@pytest.mark.parametrize("sstride,dstride", [
+    ((0,) * 5, (0,) * 5),                                                  # Fig. 5 / vLLM flash
+    ((2 * SUB, SUB, 128, 64, 1), (2 * SUB, SUB, 128, 64, 1)),              # block-major: K,V fold
+    ((3 * SUB, SUB, 128, 64, 1), (2 * SUB + 64, SUB, 128, 64, 1)),         # padded: non-contiguous
+    ((0,) * 5, (2 * SUB, SUB, 128, 64, 1)),                                # mixed orders
+    ((SUB + 128, 64 * (SUB + 128), 128, 64, 1), (0,) * 5),                 # padded KV-outer
+])
+def test_layouts_bit_exact(sstride, dstride):
+    sg = kvdgen.CacheGeom(2, 2, 64, 16, 64, kvdgen.FP16, sstride)
+    dg = kvdgen.CacheGeom(2, 2, 64, 16, 64, kvdgen.FP16, dstride)
+    pair = make_pair(sg, dg, seed=2)
+    try:
+        for kind in ("fragmented", "random", "contiguous"):
+            src, dst = _tables(kind, 20, 64, 64, seed=5)
+            pre = pair.download_dst()
+            pull_and_wait(pair, src, dst)
+            assert_layers_equal(pair.download_dst(), pair.expected(src, dst, pre))
+    finally:
+        pair.close()
+
+
+@pytest.mark.parametrize("geom", [
+    kvdgen.CacheGeom(3, 1, 16, 8, 50, kvdgen.FP8),         # 128 B spans
+    kvdgen.CacheGeom(2, 4, 128, 32, 40, kvdgen.FP32),      # 64 KiB spans: several tiles per block
+    kvdgen.CacheGeom(80, 2, 128, 16, 64, kvdgen.BF16),     # C4 shard geometry, small pool
+    kvdgen.CacheGeom(1, 1, 8, 1, 300, kvdgen.FP16),        # 16 B spans (minimum)
+])
+def test_geometries_bit_exact(geom):
+    pair = make_pair(geom, geom.with_blocks(geom.num_blocks + 7), seed=3)
+    try:
+        n = min(geom.num_blocks, 37)
+        src, dst = kvdgen.fragmented_table(n, geom.num_blocks, geom.num_blocks + 7, seed=9)
+        pull_and_wait(pair, src, dst)
+        assert_layers_equal(pair.download_dst(), pair.expected(src, dst))
+    finally:
+        pair.close()
+
+
+@pytest.mark.parametrize("variant", [kvd.VARIANT_LSU, kvd.VARIANT_LSU32, kvd.VARIANT_CE])
+@pytest.mark.parametrize("tile", [512, 4096, 16384, 65536])
+def test_variants_and_tiles(variant, tile):
+    g = kvdgen.CacheGeom(4, 4, 64, 16, 96, kvdgen.FP16)   # 8 KiB spans
+    pair = make_pair(g, g, seed=4)
+    try:
+        pair.peer.set(kvd.OPT_VARIANT, variant).set(kvd.OPT_TILE_BYTES, tile)
+        src, dst = kvdgen.fragmented_table(60, 96, 96, seed=tile)
+        info = pull_and_wait(pair, src, dst)
+        assert info["variant"] == variant
+        assert_layers_equal(pair.download_dst(), pair.expected(src, dst))
+    finally:
+        pair.close()
+
+
+@pytest.mark.parametrize("threads,max_ctas", [(128, 1), (1024, 3), (512, 0), (256, 7)])
+def test_grid_shapes(threads, max_ctas):
+    pair = make_pair(C1, C1, seed=5)
+    try:
+        pair.peer.set(kvd.OPT_THREADS, threads).set(kvd.OPT_MAX_CTAS, max_ctas)
+        src, dst = kvdgen.random_table(N_C1, 64, 64, seed=2)
+        info = pull_and_wait(pair, src, dst)
+        if max_ctas:
+            assert info["ctas"] <= max_ctas
+        assert_layers_equal(pair.download_dst(), pair.expected(src, dst))
+    finally:
+        pair.close()
+
+
+def test_coalesce_off_same_bytes():
+    """E10 ablation switch: coalescing changes the descriptor count, never the bytes."""
+    pair = make_pair(C1, C1, seed=6)
+    try:
+        src, dst = kvdgen.contiguous_table(N_C1, 3, 40)
+        info_on = pull_and_wait(pair, src, dst)
+        assert info_on["runs"] == 1
+        pair.upload_dst(pair.dst_host)
+        pair.peer.set(kvd.OPT_COALESCE, 0)
+        info_off = pull_and_wait(pair, src, dst)
+        assert info_off["runs"] == N_C1
+        assert_layers_equal(pair.download_dst(), pair.expected(src, dst))
+    finally:
+        pair.close()
+
+
+def test_run_table_in_device_memory():
+    """More runs than fit in kernel parameters (> 2016): the per-slot device
+    run table path."""
+    g = kvdgen.CacheGeom(2, 1, 8, 1, 6000, kvdgen.FP16)
+    pair = make_pair(g, g, seed=7)
+    try:
+        src, dst = kvdgen.random_table(5000, 6000, 6000, seed=3)
+        info = pull_and_wait(pair, src, dst)
+        assert info["runs"] > 2016
+        assert_layers_equal(pair.download_dst(), pair.expected(src, dst))
+        # again (slot reuse with an already-grown buffer)
+        src2, dst2 = kvdgen.random_table(4000, 6000, 6000, seed=4)
+        pre = pair.download_dst()
+        pull_and_wait(pair, src2, dst2)
+        assert_layers_equal(pair.download_dst(), pair.expected(src2, dst2, pre))
+    finally:
+        pair.close()
+
+
+def test_n_zero_completes_without_bytes():
+    pair = make_pair(C1, C1, seed=8)
+    try:
+        info = pull_and_wait(pair, [], [])
+        assert info["bytes"] == 0 and info["launches"] == 1
+        assert_layers_equal(pair.download_dst(), pair.dst_host)
+    finally:
+        pair.close()
+
+
+@pytest.mark.parametrize("src,dst,status", [
+    ([0, 64], [1, 2], kvd.ERANGE), ([0, 1], [1, 64], kvd.ERANGE), ([-1], [3], kvd.ERANGE),
+    ([0, 1], [3, 3], kvd.EINVAL),
+])
+def test_errors_change_nothing(src, dst, status):
+    pair = make_pair(C1, C1, seed=9)
+    try:
+        with pytest.raises(kvd.KvdError) as ei:
+            pair.peer.pull(next_request_id(), src, dst)
+        assert ei.value.status == status
+        torch.cuda.synchronize()
+        assert_layers_equal(pair.download_dst(), pair.dst_host)
+    finally:
+        pair.close()
+
+
+def test_busy_and_unknown_request():
+    pair = make_pair(C1, C1, seed=10)
+    try:
+        rid = next_request_id()
+        src, dst = kvdgen.contiguous_table(4)
+        pair.peer.pull(rid, src, dst)
+        with pytest.raises(kvd.KvdError) as ei:
+            pair.peer.pull(rid, src, dst)
+        assert ei.value.status == kvd.EBUSY
+        pair.peer.wait(rid)
+        with pytest.raises(kvd.KvdError) as ei:
+            pair.peer.poll(rid)                       # retired after done
+        assert ei.value.status == kvd.EINVAL
+        pair.peer.pull(rid, src, dst)                 # id may be reused
+        pair.peer.wait(rid)
+    finally:
+        pair.close()
+
+
+def test_incompatible_caches_rejected():
+    a = make_pair(C1, C1, seed=11)
+    try:
+        other = kvdgen.CacheGeom(2, 2, 64, 8, 64, kvdgen.FP16)      # block_size differs
+        from gpu_helpers import cache_for
+        c = cache_for(other, 0)
+        with pytest.raises(kvd.KvdError) as ei:
+            c.open_peer(a.src.export())
+        assert ei.value.status == kvd.ELAYOUT
+        c.close()
+    finally:
+        a.close()
+
+
+def test_many_requests_in_flight_then_poll():
+    """Several requests on one stream, polled afterwards in reverse order."""
+    g = kvdgen.CacheGeom(2, 2, 64, 16, 256, kvdgen.FP16)
+    pair = make_pair(g, g, seed=12)
+    try:
+        tables = kvdgen.disjoint_fragmented_tables([16, 5, 30, 1, 9, 40], 256, 256, seed=1)
+        rids = []
+        for s, d in tables:
+            rid = next_request_id()
+            pair.peer.pull(rid, s, d)
+            rids.append(rid)
+        for rid in reversed(rids):
+            pair.peer.wait(rid)
+        exp = pair.dst_host
+        for s, d in tables:
+            exp = pair.expected(s, d, exp)
+        assert_layers_equal(pair.download_dst(), exp)
+    finally:
+        pair.close()
+
+
+def test_completion_flag_never_precedes_data():
+    """P4: the first time kvd_poll_done returns 1 the host immediately reads
+    the destination blocks on ANOTHER stream; they must already hold the
+    pulled bytes.  Random n <= 64, C1-like geometry, thousands of pulls."""
+    g = kvdgen.CacheGeom(2, 2, 64, 16, 256, kvdgen.FP16)
+    pair = make_pair(g, g, seed=13)
+    side = torch.cuda.Stream()
+    rng = np.random.default_rng(0)
+    span = pair.src.span_bytes
+    try:
+        src_view = [torch.from_numpy(h).view(2, 256, span) for h in pair.src_host]
+        for it in range(3000):
+            n = int(rng.integers(1, 65))
+            s = rng.choice(256, n, replace=False).astype(np.int32)
+            d = rng.choice(256, n, replace=False).astype(np.int32)
+            rid = next_request_id()
+            pair.peer.pull(rid, s, d)
+            while not pair.peer.poll(rid):
+                pass
+            with torch.cuda.stream(side):
+                got = [t.view(2, 256, span)[:, torch.from_numpy(d).long().cuda()].cpu()
+                       for t in pair.dst.layers]
+            for l in range(g.num_layers):
+                want = src_view[l][:, torch.from_numpy(s).long()]
+                assert torch.equal(got[l], want), f"iteration {it} layer {l}: flag before data"
+    finally:
+        pair.close()
+
+
+@pytest.mark.parametrize("single_allocation", [False, True])
+def test_c2_full_size_sampled(single_allocation):
+    """C2 at full size (32 layers x 32 heads x 128, 8K tokens = 4 GiB) in the
+    launch configuration bench.py times; checked on sampled elements
+    against the oracle's element addresses, plus a whole-request property
+    check (every pulled block equals its source block) on the device."""
+    from gpu_helpers import cache_for
+    from oracle import oracle
+    g = kvdgen.C2
+    n = kvdgen.blocks_for(kvdgen.C2_TOKENS, g.block_size)
+    src = cache_for(g, 0, single_allocation)
+    dst = cache_for(g, 0, single_allocation)
+    for l in range(g.num_layers):
+        kvdgen.torch_fill_random_(src.layers[l], 1000 + l)
+        kvdgen.torch_fill_random_(dst.layers[l], 2000 + l)
+    peer = dst.open_peer(src.export())
+    try:
+        s_ids, d_ids = kvdgen.fragmented_table(n, g.num_blocks, g.num_blocks, seed=1)
+        rng = np.random.default_rng(5)
+        untouched = np.setdiff1d(np.arange(g.num_blocks), d_ids)[:16]
+        span = src.span_bytes
+        before = {l: dst.layers[l].view(2, g.num_blocks, span)[:, torch.from_numpy(untouched).long().cuda()].cpu()
+                  for l in (0, g.num_layers - 1)}
+        rid = next_request_id()
+        peer.pull(rid, s_ids, d_ids)
+        peer.wait(rid)
+        info = peer.info()
+        assert info["bytes"] == 4 * 2**30
+        # sampled elements, addresses from the oracle's dot product
+        e = g.elem_bytes
+        for _ in range(2000):
+            l = int(rng.integers(g.num_layers)); i = int(rng.integers(n))
+            kv, t, h, d = (int(rng.integers(2)), int(rng.integers(16)), int(rng.integers(32)),
+                           int(rng.integers(128)))
+            so = oracle.c_layer_element_offset((0,) * 5, g.num_blocks, 16, 32, 128, e,
+                                               int(s_ids[i]), kv, t, h, d)
+            do = oracle.c_layer_element_offset((0,) * 5, g.num_blocks, 16, 32, 128, e,
+                                               int(d_ids[i]), kv, t, h, d)
+            assert torch.equal(dst.layers[l][do:do + e], src.layers[l][so:so + e])
+        # whole request on device + untouched blocks
+        si = torch.from_numpy(s_ids).long().cuda()
+        di = torch.from_numpy(d_ids).long().cuda()
+        for l in range(g.num_layers):
+            assert torch.equal(dst.layers[l].view(2, g.num_blocks, span)[:, di],
+                               src.layers[l].view(2, g.num_blocks, span)[:, si]), l
+        for l, b in before.items():
+            now = dst.layers[l].view(2, g.num_blocks, span)[:, torch.from_numpy(untouched).long().cuda()].cpu()
+            assert torch.equal(now, b)
+    finally:
+        peer.close()
+        dst.close()
+        src.close()
+
+
+def test_c4_shard_full_size_bit_exact():
+    """C4 shard (80 layers x 2 heads x 128, bf16, 8K tokens = 640 MiB) fully
+    compared with the oracle on host copies."""
+    g = kvdgen.C4
+    n = kvdgen.blocks_for(kvdgen.C4_TOKENS, g.block_size)
+    pair = make_pair(g, g, seed=14)
+    try:
+        s_ids, d_ids = kvdgen.fragmented_table(n, g.num_blocks, g.num_blocks, seed=4)
+        info = pull_and_wait(pair, s_ids, d_ids)
+        assert info["bytes"] == 671_088_640
+        assert_layers_equal(pair.download_dst(), pair.expected(s_ids, d_ids))
+    finally:
+        pair.close()
+
+
+@pytest.mark.gpu2
+def test_two_gpus_same_process():
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs")
+    pair = make_pair(C1.with_blocks(512), C1.with_blocks(512), seed=15, src_dev=0, dst_dev=1)
+    try:
+        for kind in ("contiguous", "fragmented", "random"):
+            src, dst = _tables(kind, 300, 512, 512, seed=3)
+            pre = pair.download_dst()
+            torch.cuda.set_device(1)
+            pull_and_wait(pair, src, dst)
+            assert_layers_equal(pair.download_dst(), pair.expected(src, dst, pre))
+    finally:
+        torch.cuda.set_device(0)
+        pair.close()
