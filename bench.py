@@ -1,0 +1,487 @@
+#!/usr/bin/env python
+"""bench.py -- KV pull GB/s per GPU pair and p50 per-request transfer latency
+(BASELINE.json metric) for KVDirect's pull path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c1|c4]
+                    [--table fragmented|contiguous|worst] [--impl kvd|reference]
+
+N = 1: no NVLink pair exists on one GPU, so the prefill and decode caches
+share cuda:0 (loopback pull, HBM-bound); this is stated in config.pairing.
+N >= 2 (torchrun, one process per GPU): ranks [0, N/2) hold prefill caches,
+ranks [N/2, N) hold decode caches; decode rank N/2 + k pulls from prefill
+rank k (the paper's rail rule "GPU i ... only with GPU i") over
+NVLink 5 / NVSwitch through CUDA IPC.  No collective on the data path.
+
+A step = one pass of the per-request hot path over
+one C2 request on every pair: kvd_pull (validate + coalesce + one launch)
+and kvd_poll_done until the device-side completion word flips.  Rows a1-a2
+(register, export/open) are the paper's one-time Connect() and run before
+the timed region.  `value` = bytes pulled by all pairs / device time of the
+K steps (CUDA events on the pull stream, max over ranks); `e2e` = the same
+bytes / host wall time from kvd_pull entry to completion observed.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import kvdgen  # noqa: E402
+
+METRIC = "KV pull GB/s per GPU pair vs 900 GB/s NVLink; p50 per-request transfer latency"
+NVLINK_NOMINAL_GBS = 900.0
+NVLINK_MEASURED_GBS = 770.0   # B200_PROFILING.md: measured peer copy per direction
+
+
+# ---------------------------------------------------------------------------
+# helpers
+# ---------------------------------------------------------------------------
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "MEASURED_PEAKS.json"
+    except Exception:
+        return {"hbm_gbs": 6650.0}, "fallback B200_PROFILING.md"
+
+
+def nearest_rank(xs, q):
+    """Nearest-rank percentile."""
+    s = sorted(xs)
+    if not s:
+        return None
+    k = max(1, int(np.ceil(q / 100.0 * len(s))))
+    return s[k - 1]
+
+
+class ClockSampler:
+    """Samples SM clock and clock-event reasons through NVML during the
+    timed region (B200_PROFILING.md clocks line)."""
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, device_index: int, period_s: float = 0.005):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            phys = int(vis.split(",")[device_index]) if vis else device_index
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(phys)
+            self._nvml = pynvml
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nvml = None
+        self.period = period_s
+
+    def _run(self):
+        n = self._nvml
+        while not self._stop.is_set():
+            try:
+                self.samples.append(n.nvmlDeviceGetClockInfo(self._h, n.NVML_CLOCK_SM))
+                r = n.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self._nvml:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "samples": len(self.samples),
+                "reasons": sorted(self.reasons)}
+
+
+def workload(config: str, table: str):
+    """(geometry, tokens, src_ids, dst_ids, description) for a config."""
+    if config == "c1":
+        g, tokens = kvdgen.C1, kvdgen.C1_TOKENS
+    elif config == "c4":
+        g, tokens = kvdgen.C4, kvdgen.C4_TOKENS
+    else:
+        g, tokens = kvdgen.C2, kvdgen.C2_TOKENS
+    n = kvdgen.blocks_for(tokens, g.block_size)
+    if table == "contiguous":
+        s, d = kvdgen.contiguous_table(n, 0, g.num_blocks - n)
+    elif table == "worst":
+        s, d = kvdgen.fixed_run_table(n, 1, g.num_blocks, g.num_blocks, seed=1)
+    else:
+        s, d = kvdgen.fragmented_table(n, g.num_blocks, g.num_blocks, seed=1)
+    names = {"c1": "C1 tiny (2 layers, 2 KV heads, head_dim 64, block 16, fp16), 256-token request",
+             "c2": "C2 Llama-2-7B KV cache (32 layers, 32 KV heads, head_dim 128, block 16, fp16), "
+                   "one 8K-token request",
+             "c4": "C4 Llama-3-70B TP=4 shard (80 layers, 2 KV heads/shard, head_dim 128, block 16, "
+                   "bf16), one 8K-token request per shard"}
+    return g, tokens, s, d, names.get(config, names["c2"])
+
+
+def cpu_oracle_sample(target_s: float = 12.0):
+    """Time the CPU oracle (oracle/kvd_oracle.c, single thread, as it stands)
+    on a bounded sample of the C2 workload: C2 geometry, a fragmented request
+    of k blocks drawn from pools of 2k blocks, k chosen to take ~target_s."""
+    from oracle import oracle
+    g = kvdgen.C2
+
+    def run(k):
+        nb = 2 * k
+        lb = oracle.layer_nbytes((0,) * 5, nb, g.block_size, g.num_kv_heads, g.head_dim, 2)
+        src = [kvdgen.random_bytes(lb, 10 + l) for l in range(g.num_layers)]
+        dst = [np.zeros(lb, np.uint8) for _ in range(g.num_layers)]
+        s, d = kvdgen.fragmented_table(k, nb, nb, seed=2)
+        t = time.perf_counter()
+        rc = oracle.pull(src, (0,) * 5, nb, dst, (0,) * 5, nb, g.num_kv_heads, g.head_dim,
+                         g.block_size, 2, s, d)
+        dt = time.perf_counter() - t
+        assert rc == 0
+        return dt, k * g.num_layers * 2 * g.block_size * g.num_kv_heads * g.head_dim * 2
+
+    dt, b = run(2)
+    k = int(max(2, min(128, 2 * target_s / max(dt, 1e-3))))
+    dt, b = run(k)
+    return {"value": round(b / dt / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+            "seconds": round(dt, 2),
+            "sample": f"C2 geometry, fragmented {k}-block request ({b / 2**20:.0f} MiB) from "
+                      f"{2 * k}-block pools, oracle/kvd_oracle.c element loop, 1 thread"}
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the CPU oracle (tier rule: the oracle is the reference)
+# ---------------------------------------------------------------------------
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from oracle import oracle
+    g, tokens, _, _, desc = workload(args.config, args.table)
+    k = 4 if args.config != "c1" else kvdgen.blocks_for(tokens, g.block_size)
+    nb = max(2 * k, 8)
+    lb = oracle.layer_nbytes((0,) * 5, nb, g.block_size, g.num_kv_heads, g.head_dim,
+                             g.elem_bytes)
+    src = [kvdgen.random_bytes(lb, 10 + l) for l in range(g.num_layers)]
+    dst = [np.zeros(lb, np.uint8) for _ in range(g.num_layers)]
+    s, d = kvdgen.fragmented_table(k, nb, nb, seed=2)
+    per = k * g.num_layers * 2 * g.block_size * g.num_kv_heads * g.head_dim * g.elem_bytes
+
+    def step():
+        rc = oracle.pull(src, (0,) * 5, nb, dst, (0,) * 5, nb, g.num_kv_heads, g.head_dim,
+                         g.block_size, g.elem_bytes, s, d)
+        assert rc == 0
+
+    for _ in range(args.warmup):
+        step()
+    lat = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        step()
+        lat.append(time.perf_counter() - t)
+    dt = time.perf_counter() - t0
+    value = per * args.steps / dt / 1e9
+    sample = (f"{desc}: bounded sample of {k} blocks ({per / 2**20:.1f} MiB) per step from "
+              f"{nb}-block host pools, oracle/kvd_oracle.c element loop, 1 thread")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": desc, "sample_blocks": k},
+        "p50_latency_ms": round(nearest_rank(lat, 50) * 1e3, 3),
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": 1,
+                         "kind": "oracle", "sample": sample},
+        "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# the pull arm
+# ---------------------------------------------------------------------------
+
+def traffic_from_profile(config: str):
+    """dram bytes per launch of the pull kernel from the committed ncu
+    --set full summary (profiles/ncu_pull_<config>.json), else None."""
+    p = os.path.join(ROOT, "profiles", f"ncu_pull_{config}.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def run_kvd(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_2501_14743_b200 import kvd
+    from paper_2501_14743_b200.torch_cache import PagedCache
+
+    torch.cuda.set_device(local_rank)
+    dev = local_rank
+    g, tokens, s_ids, d_ids, desc = workload(args.config, args.table)
+    n = len(s_ids)
+    multi = world > 1
+    if multi:
+        half = world // 2
+        role = "prefill" if rank < half else "decode"
+        pairs = half
+        gloo = dist.new_group(backend="gloo")
+    else:
+        role, pairs, gloo = "both", 1, None
+
+    def new_cache(seed):
+        c = PagedCache(g.num_layers, g.num_kv_heads, g.head_dim, g.block_size, g.num_blocks,
+                       g.dtype, g.stride, dev)
+        for l, t in enumerate(c.layers):
+            kvdgen.torch_fill_random_(t, seed * 1000 + l)
+        return c
+
+    src = new_cache(1 + rank) if role in ("prefill", "both") else None
+    dst = new_cache(100 + rank) if role in ("decode", "both") else None
+    torch.cuda.synchronize()
+
+    # row a2: one-time tensor-centric exchange (Connect())
+    if multi:
+        blobs = [None] * world
+        dist.all_gather_object(blobs, src.export() if src else None, group=gloo)
+        peer_blob = blobs[rank - half] if role == "decode" else None
+    else:
+        peer_blob = src.export()
+    peer = dst.open_peer(peer_blob) if dst else None
+    if peer:
+        if args.variant:
+            peer.set(kvd.OPT_VARIANT, {"lsu": 1, "lsu32": 2, "ce": 3}[args.variant])
+        if args.tile:
+            peer.set(kvd.OPT_TILE_BYTES, args.tile)
+        if args.threads:
+            peer.set(kvd.OPT_THREADS, args.threads)
+        if args.max_ctas:
+            peer.set(kvd.OPT_MAX_CTAS, args.max_ctas)
+        if args.no_coalesce:
+            peer.set(kvd.OPT_COALESCE, 0)
+
+    stream = torch.cuda.Stream(dev)
+    rid = [rank * 10_000_000]
+
+    def one_pull():
+        rid[0] += 1
+        t0 = time.perf_counter_ns()
+        peer.pull(rid[0], s_ids, d_ids, stream)
+        while not peer.poll(rid[0]):
+            pass
+        return time.perf_counter_ns() - t0
+
+    def barrier():
+        torch.cuda.synchronize()
+        if multi:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        if peer:
+            one_pull()
+    barrier()
+
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(K)] if peer else []
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    lat_ns = []
+    sampler = ClockSampler(dev)
+    barrier()
+    with sampler:
+        wall0 = time.perf_counter()
+        if peer:
+            t_start.record(stream)
+            for k in range(K):
+                ev[k][0].record(stream)
+                rid[0] += 1
+                t0 = time.perf_counter_ns()
+                peer.pull(rid[0], s_ids, d_ids, stream)
+                ev[k][1].record(stream)
+                while not peer.poll(rid[0]):
+                    pass
+                lat_ns.append(time.perf_counter_ns() - t0)
+            t_end.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - wall0
+    barrier()
+
+    info = peer.info() if peer else {}
+    dev_s = t_start.elapsed_time(t_end) / 1e3 if peer else 0.0
+    kern_ms = [a.elapsed_time(b) for a, b in ev]
+    bytes_per = int(info.get("bytes", 0))
+
+    # parity of the timed configuration (checked once, after timing)
+    ok = True
+    if peer:
+        span = dst.span_bytes
+        di = torch.from_numpy(d_ids).long().cuda(dev)
+        if role == "both":
+            si = torch.from_numpy(s_ids).long().cuda(dev)
+            for l in range(g.num_layers):
+                ok = ok and torch.equal(dst.layers[l].view(2, g.num_blocks, span)[:, di],
+                                        src.layers[l].view(2, g.num_blocks, span)[:, si])
+    if multi:
+        # prefill ranks publish per-(layer, plane, block) fingerprints of the
+        # request's source blocks; decode ranks compare their destination blocks
+        def fp(cache, ids):
+            idx = torch.from_numpy(ids).long().cuda(dev)
+            w = torch.arange(1, cache.span_bytes // 8 + 1, device=f"cuda:{dev}", dtype=torch.int64)
+            return torch.stack([(cache.layers[l].view(2, g.num_blocks, -1)[:, idx]
+                                 .view(torch.int64) * w).sum(-1)
+                                for l in range(g.num_layers)]).cpu()
+        mine = fp(src, s_ids) if role == "prefill" else None
+        fps = [None] * world
+        dist.all_gather_object(fps, mine, group=gloo)
+        if role == "decode":
+            ok = bool(torch.equal(fp(dst, d_ids), fps[rank - half]))
+    oks = [None] * world if multi else [ok]
+    if multi:
+        dist.all_gather_object(oks, bool(ok), group=gloo)
+
+    # max over ranks
+    stats = {"dev_s": dev_s, "wall_s": wall if peer else 0.0, "bytes": bytes_per * K if peer else 0,
+             "kern_ms": float(np.mean(kern_ms)) if kern_ms else 0.0,
+             "lat": lat_ns, "clock": sampler.summary(), "info": info}
+    all_stats = [None] * world if multi else [stats]
+    if multi:
+        dist.all_gather_object(all_stats, stats, group=gloo)
+
+    if rank == 0:
+        dec = [s for s in all_stats if s["bytes"]]
+        t_dev = max(s["dev_s"] for s in dec)
+        t_wall = max(s["wall_s"] for s in dec)
+        total = sum(s["bytes"] for s in dec)
+        lat_all = [x for s in dec for x in s["lat"]]
+        kern = max(s["kern_ms"] for s in dec)
+        info0 = dec[0]["info"]
+        per_launch = info0["bytes"]
+        peaks, peak_src = measured_peaks()
+        if multi:
+            roof = {"bound": "nvlink", "achieved": round(per_launch / (kern / 1e3) / 1e9, 1),
+                    "peak": NVLINK_MEASURED_GBS, "unit": "GB/s",
+                    "frac": round(per_launch / (kern / 1e3) / 1e9 / NVLINK_MEASURED_GBS, 4),
+                    "frac_of_nominal_900": round(per_launch / (kern / 1e3) / 1e9 /
+                                                 NVLINK_NOMINAL_GBS, 4),
+                    "peak_source": "B200_PROFILING.md measured peer copy per direction "
+                                   "(nominal 900)",
+                    "algorithmic_bytes_per_launch": per_launch,
+                    "traffic": traffic_from_profile(args.config)}
+        else:
+            alg = 2 * per_launch   # loopback: every byte is read and written in the same HBM
+            roof = {"bound": "hbm", "achieved": round(alg / (kern / 1e3) / 1e9, 1),
+                    "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                    "frac": round(alg / (kern / 1e3) / 1e9 / peaks["hbm_gbs"], 4),
+                    "peak_source": peak_src + " hbm_gbs (burst copy, read+write bytes)",
+                    "algorithmic_bytes_per_launch": alg,
+                    "traffic": traffic_from_profile(args.config)}
+        clk = all_stats[world // 2 if multi else 0]["clock"]
+        out = {
+            "metric": METRIC, "value": round(total / t_dev / 1e9, 2), "unit": "GB/s",
+            "n_gpus": world, "steps": K, "warmup": args.warmup,
+            "ms_per_step": round(t_dev / K * 1e3, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {
+                "workload": desc, "table": f"{args.table} (kvdgen seed 1)", "blocks": n,
+                "runs": info0.get("runs"), "bytes_per_request": per_launch,
+                "pairs": pairs,
+                "pairing": ("loopback: prefill and decode caches on the same GPU (one GPU has "
+                            "no NVLink pair)") if not multi else
+                           f"{pairs}P:{pairs}D rail pairs, rank k -> rank {pairs}+k over NVLink 5",
+                "parallelism": "loopback" if not multi else f"{pairs}x(1P:1D)",
+                "l2": "no flush: each request moves >= 640 MiB, >> 126 MB L2",
+                "cache_dtype": "fp16" if g.dtype == kvdgen.FP16 else "bf16",
+                "variant": info0.get("variant"), "ctas": info0.get("ctas"),
+                "threads": info0.get("threads"), "tiles": info0.get("tiles"),
+            },
+            "gbs_per_pair": round(total / pairs / t_dev / 1e9, 2),
+            "frac_of_nvlink_900_per_pair": round(total / pairs / t_dev / 1e9 / NVLINK_NOMINAL_GBS,
+                                                 4),
+            "p50_latency_ms": round(nearest_rank(lat_all, 50) / 1e6, 4),
+            "p90_latency_ms": round(nearest_rank(lat_all, 90) / 1e6, 4),
+            "kernel_ms": round(kern, 4),
+            "roofline": roof,
+            "e2e": {"value": round(total / t_wall / 1e9, 2), "unit": "GB/s",
+                    "h2d_bytes_per_step": 8 * n * pairs, "d2h_bytes_per_step": 8 * pairs,
+                    "what": "host wall from kvd_pull entry (host block-id tables -> kernel "
+                            "parameters) to the host observing the pinned completion word"},
+            "gpu_launches": sum(s["info"].get("launches", 0) for s in dec) * K,
+            "parity": bool(all(oks)),
+            "clocks": clk,
+        }
+        if not multi and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_oracle_sample()
+        print(json.dumps(out), flush=True)
+
+    if peer:
+        peer.close()
+    if multi:
+        dist.barrier(group=gloo)
+    for c in (dst, src):
+        if c:
+            c.close()
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["kvd", "reference"], default="kvd")
+    ap.add_argument("--config", choices=["c1", "c2", "c4"], default="c2")
+    ap.add_argument("--table", choices=["fragmented", "contiguous", "worst"], default="fragmented")
+    ap.add_argument("--variant", choices=["lsu", "lsu32", "ce"], default=None)
+    ap.add_argument("--tile", type=int, default=0)
+    ap.add_argument("--threads", type=int, default=0)
+    ap.add_argument("--max-ctas", type=int, default=0)
+    ap.add_argument("--no-coalesce", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if world != args.gpus:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if world % 2:
+            raise SystemExit("N > 1 must be even (prefill/decode pairs)")
+    run_kvd(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
