@@ -159,7 +159,7 @@ def cpu_oracle_sample(target_s: float = 12.0):
         return dt, k * g.num_layers * 2 * g.block_size * g.num_kv_heads * g.head_dim * 2
 
     dt, b = run(2)
-    k = int(max(2, min(128, 2 * target_s / max(dt, 1e-3))))
+    k = int(max(2, min(256, 2 * target_s / max(dt, 1e-3))))
     dt, b = run(k)
     return {"value": round(b / dt / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
             "seconds": round(dt, 2),
@@ -220,10 +220,12 @@ def run_reference(args, rank, world):
 # the pull arm
 # ---------------------------------------------------------------------------
 
-def traffic_from_profile(config: str):
+def traffic_from_profile(config: str, nvlink: bool):
     """dram bytes per launch of the pull kernel from the committed ncu
-    --set full summary (profiles/ncu_pull_<config>.json), else None."""
-    p = os.path.join(ROOT, "profiles", f"ncu_pull_{config}.json")
+    --set full summary (profiles/ncu_pull_<config>[_nvlink].json), else None.
+    For the NVLink case this is the decode GPU's DRAM only (the prefill
+    GPU's reads are not visible to the decode process's counters)."""
+    p = os.path.join(ROOT, "profiles", f"ncu_pull_{config}{'_nvlink' if nvlink else ''}.json")
     try:
         with open(p) as f:
             return json.load(f).get("dram_bytes_per_launch")
@@ -388,7 +390,7 @@ def run_kvd(args, rank, world, local_rank):
                     "peak_source": "B200_PROFILING.md measured peer copy per direction "
                                    "(nominal 900)",
                     "algorithmic_bytes_per_launch": per_launch,
-                    "traffic": traffic_from_profile(args.config)}
+                    "traffic": traffic_from_profile(args.config, True)}
         else:
             alg = 2 * per_launch   # loopback: every byte is read and written in the same HBM
             roof = {"bound": "hbm", "achieved": round(alg / (kern / 1e3) / 1e9, 1),
@@ -396,7 +398,7 @@ def run_kvd(args, rank, world, local_rank):
                     "frac": round(alg / (kern / 1e3) / 1e9 / peaks["hbm_gbs"], 4),
                     "peak_source": peak_src + " hbm_gbs (burst copy, read+write bytes)",
                     "algorithmic_bytes_per_launch": alg,
-                    "traffic": traffic_from_profile(args.config)}
+                    "traffic": traffic_from_profile(args.config, False)}
         clk = all_stats[world // 2 if multi else 0]["clock"]
         out = {
             "metric": METRIC, "value": round(total / t_dev / 1e9, 2), "unit": "GB/s",
