@@ -233,6 +233,106 @@ def traffic_from_profile(config: str, nvlink: bool):
         return None
 
 
+def nccl_baselines(args, g, s_ids, d_ids, src, dst, role, rank, half, dev, gloo, fingerprint):
+    """The measured baseline (north_star: "NCCL send/recv is kept only as the
+    measured baseline"), same caches and block tables as the pull.
+
+    N1 = the message-passing flow of fig:diff(a): decode sends the
+    wanted block ids (step 1), prefill gathers the blocks into a staging
+    buffer with a kernel (2) and ncclSend's it (3), decode ncclRecv's and
+    scatters it into its paged cache (4).  Whole request staged at once.
+    N2 = grouped per-segment send/recv (ncclGroupStart/End via
+    batch_isend_irecv), no staging: one send/recv per contiguous (layer,
+    K/V, run) segment straight between the paged caches.
+    Each is timed as host wall per request (max over ranks) and parity-checked
+    (the decode cache is scribbled before each baseline)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2501_14743_b200 import kvd
+    n = len(s_ids)
+    span = (src or dst).span_bytes
+    nb = g.num_blocks
+    per = g.num_layers * 2 * n * span
+    peer_rank = rank + half if role == "prefill" else rank - half
+    stream = torch.cuda.current_stream(dev)
+    ids_dev = torch.empty(n, dtype=torch.int32, device=f"cuda:{dev}")
+    ids_host = torch.from_numpy(np.ascontiguousarray(s_ids, dtype=np.int32)).pin_memory()
+    runs = kvd.kvd_plan(s_ids, d_ids, nb, nb)
+    out = {}
+
+    def segments(cache, side):
+        views = []
+        for l in range(g.num_layers):
+            layer = cache.layers[l]
+            for p in range(2):
+                for r in runs:
+                    b0 = int(r[side])
+                    off = p * nb * span + b0 * span
+                    views.append(layer[off:off + int(r[2]) * span])
+        return views
+
+    def scribble():
+        if role == "decode":
+            for l, t in enumerate(dst.layers):
+                kvdgen.torch_fill_random_(t, 777 + l)
+        torch.cuda.synchronize(dev)
+
+    staging = torch.empty(per, dtype=torch.uint8, device=f"cuda:{dev}")
+
+    def n1():
+        if role == "decode":
+            ids_dev.copy_(ids_host, non_blocking=True)
+            dist.send(ids_dev, peer_rank)
+            dist.recv(staging, peer_rank)
+            kvd.kvd_scatter(dst.handle, d_ids, staging.data_ptr(), stream.cuda_stream)
+        else:
+            dist.recv(ids_dev, peer_rank)
+            want = ids_dev.cpu().numpy()          # the RPC'd block ids drive the gather
+            kvd.kvd_gather(src.handle, want, staging.data_ptr(), stream.cuda_stream)
+            dist.send(staging, peer_rank)
+        torch.cuda.synchronize(dev)
+
+    seg_views = segments(src, 0) if role == "prefill" else segments(dst, 1)
+
+    def n2():
+        if role == "decode":
+            ids_dev.copy_(ids_host, non_blocking=True)
+            dist.send(ids_dev, peer_rank)
+            ops = [dist.P2POp(dist.irecv, v, peer_rank) for v in seg_views]
+        else:
+            dist.recv(ids_dev, peer_rank)
+            ops = [dist.P2POp(dist.isend, v, peer_rank) for v in seg_views]
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+        torch.cuda.synchronize(dev)
+
+    for name, fn, steps in (("n1_gather_send_recv_scatter", n1, args.steps),
+                            ("n2_grouped_segment_send_recv", n2, max(3, min(args.steps, 10)))):
+        scribble()
+        for _ in range(2):
+            fn()
+        dist.barrier()
+        lat = []
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            t = time.perf_counter()
+            fn()
+            lat.append(time.perf_counter() - t)
+        wall = time.perf_counter() - t0
+        dist.barrier()
+        ok = True
+        mine = fingerprint(src, s_ids) if role == "prefill" else None
+        fps = [None] * dist.get_world_size()
+        dist.all_gather_object(fps, mine, group=gloo)
+        if role == "decode":
+            ok = bool(torch.equal(fingerprint(dst, d_ids), fps[peer_rank]))
+        out[name] = {"wall_s": wall, "steps": steps, "bytes": per * steps if role == "decode" else 0,
+                     "lat": lat, "ok": ok,
+                     "segments": len(seg_views) if name.startswith("n2") else 1}
+    del staging
+    return out
+
+
 def run_kvd(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -363,10 +463,14 @@ def run_kvd(args, rank, world, local_rank):
     if multi:
         dist.all_gather_object(oks, bool(ok), group=gloo)
 
+    base = {}
+    if multi and not args.no_nccl:
+        base = nccl_baselines(args, g, s_ids, d_ids, src, dst, role, rank, half, dev, gloo, fp)
+
     # max over ranks
     stats = {"dev_s": dev_s, "wall_s": wall if peer else 0.0, "bytes": bytes_per * K if peer else 0,
              "kern_ms": float(np.mean(kern_ms)) if kern_ms else 0.0,
-             "lat": lat_ns, "clock": sampler.summary(), "info": info}
+             "lat": lat_ns, "clock": sampler.summary(), "info": info, "base": base}
     all_stats = [None] * world if multi else [stats]
     if multi:
         dist.all_gather_object(all_stats, stats, group=gloo)
@@ -433,6 +537,24 @@ def run_kvd(args, rank, world, local_rank):
             "parity": bool(all(oks)),
             "clocks": clk,
         }
+        if multi and not args.no_nccl:
+            nb_out = {}
+            for name in ("n1_gather_send_recv_scatter", "n2_grouped_segment_send_recv"):
+                rs = [s["base"][name] for s in all_stats if s["base"] and s["base"][name]["bytes"]]
+                t = max(r["wall_s"] for r in rs)
+                tot = sum(r["bytes"] for r in rs)
+                lat = [x for r in rs for x in r["lat"]]
+                oks_b = [s["base"][name]["ok"] for s in all_stats if s["base"]]
+                nb_out[name] = {"value": round(tot / t / 1e9, 2), "unit": "GB/s",
+                                "gbs_per_pair": round(tot / pairs / t / 1e9, 2),
+                                "p50_latency_ms": round(nearest_rank(lat, 50) * 1e3, 4),
+                                "steps": rs[0]["steps"], "segments_per_request": rs[0]["segments"],
+                                "parity": bool(all(oks_b))}
+            nb_out["kvd_pull_e2e_vs_n1"] = round(
+                out["e2e"]["value"] / nb_out["n1_gather_send_recv_scatter"]["value"], 3)
+            nb_out["what"] = ("NCCL 2.28 send/recv via torch.distributed on the same caches and "
+                              "block tables; host wall per request incl. the block-id message")
+            out["nccl_baseline"] = nb_out
         if not multi and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_oracle_sample()
         print(json.dumps(out), flush=True)
@@ -460,6 +582,7 @@ def main():
     ap.add_argument("--max-ctas", type=int, default=0)
     ap.add_argument("--no-coalesce", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-nccl", action="store_true", help="skip the NCCL send/recv baselines")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

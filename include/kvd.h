@@ -118,7 +118,9 @@ typedef enum {
   KVD_VARIANT_AUTO = 0,  /* library choice */
   KVD_VARIANT_LSU = 1,   /* SM loads 16 B/lane from the peer, stores locally (default) */
   KVD_VARIANT_LSU32 = 2, /* 32 B/lane (sm_100 256-bit ld/st); needs 32 B alignment */
-  KVD_VARIANT_CE = 3     /* copy engine: one cudaMemcpyAsync per segment (comparator only) */
+  KVD_VARIANT_CE = 3,    /* copy engine: one cudaMemcpyAsync per segment (comparator only) */
+  KVD_VARIANT_TMA = 4    /* one lane per warp runs an S-stage cp.async.bulk ring peer HBM ->
+                            shared memory -> local HBM; saturates NVLink with few SMs */
 } kvd_variant;
 
 typedef enum {
@@ -126,7 +128,10 @@ typedef enum {
   KVD_OPT_TILE_BYTES = 1,   /* bytes per warp work item, multiple of 512 (default 16384) */
   KVD_OPT_COALESCE = 2,     /* 1 (default) merge bi-contiguous runs; 0 one run per block (E10 ablation) */
   KVD_OPT_VARIANT = 3,      /* kvd_variant */
-  KVD_OPT_THREADS = 4       /* threads per CTA: 128..1024, multiple of 32 (default 512) */
+  KVD_OPT_THREADS = 4,      /* threads per CTA: multiple of 32; LSU 128..1024 (default 512);
+                               TMA: threads/32 pipes per CTA, 32..1024 (default 96) */
+  KVD_OPT_STAGES = 5        /* TMA ring depth per pipe, 2..8 (default 4); pipes * stages *
+                               tile_bytes must fit in 225 KiB of shared memory */
 } kvd_option;
 
 typedef struct kvd_cache_s* kvd_cache;
@@ -185,8 +190,11 @@ KVD_API kvd_status kvd_unregister_cache(kvd_cache cache);
  * (memory not legacy-IPC capable, e.g. VMM/expandable segments). */
 KVD_API kvd_status kvd_export_handle(kvd_cache cache, void* blob, size_t* blob_len);
 
-/* Import a prefill cache's blob on the decode side and bind it to the local
- * destination cache.  Checks compatibility (same layers, heads, head_dim,
+/* Import a peer cache's blob and bind it to a local cache.  For the pull
+ * path (the product) the decode process imports the prefill cache's blob and
+ * `local_dst` is its decode cache; for the push variant (kvd_push) the
+ * prefill process imports the decode cache's blob and `local_dst` is its
+ * prefill cache.  Checks compatibility (same layers, heads, head_dim,
  * block_size, element size; B/KV strides and num_blocks may differ)
  * -> KVD_ELAYOUT; maps each allocation with cudaIpcOpenMemHandle on the
  * local device (or, for a blob exported by this same process, uses the raw
@@ -222,6 +230,18 @@ KVD_API kvd_status kvd_pull(kvd_peer peer, uint64_t request_id, const int32_t* s
  * *done = 0 while in flight.  Makes no CUDA call (reads a pinned flag).
  * Errors: KVD_EINVAL for an unknown request id. */
 KVD_API kvd_status kvd_poll_done(kvd_peer peer, uint64_t request_id, int* done);
+
+/* Push variant (§4.3 push mode, P:L402,
+ * fig:push_pull): launched on the PREFILL GPU, copies local blocks
+ * src_ids[i] of the peer's local cache into REMOTE blocks dst_ids[i] of the
+ * imported (decode) cache with NVLink stores, all layers and K/V in one
+ * launch.  Same validation, coalescing, errors and completion slots as
+ * kvd_pull (the completion word lives in the pusher's host memory; the
+ * caller tells the decode side).  The paper pushes layer by layer while
+ * prefill computes; this variant pushes the finished request in one shot
+ * so the two transfer directions are compared on equal terms. */
+KVD_API kvd_status kvd_push(kvd_peer peer, uint64_t request_id, const int32_t* src_ids,
+                            const int32_t* dst_ids, uint32_t n, void* stream);
 
 /* Spin on kvd_poll_done until done or `timeout_us` elapses (KVD_EBUSY). */
 KVD_API kvd_status kvd_wait_done(kvd_peer peer, uint64_t request_id, int64_t timeout_us);

@@ -409,6 +409,10 @@ struct kvd_peer_s {
   uint32_t max_ctas = 0;
   uint32_t tile_bytes = 16384;
   uint32_t threads = 512;
+  bool threads_set = false;                 // else per-variant default (LSU 512, TMA 96 / auto 32)
+  bool tile_set = false;                    // else 16 KiB (auto TMA: 32 KiB)
+  uint32_t stages = 4;                      // TMA ring depth (auto TMA: 6)
+  bool stages_set = false;
   int coalesce = 1;
   int variant = KVD_VARIANT_AUTO;
   int sm_count = 148;
@@ -767,19 +771,27 @@ kvd_status kvd_peer_set(kvd_peer p, int option, int64_t value) {
       if (value < 512 || value % 512 || value > (1 << 24))
         return fail(KVD_EINVAL, "tile_bytes must be a multiple of 512 in [512, 16 MiB]");
       p->tile_bytes = (uint32_t)value;
+      p->tile_set = true;
       return KVD_OK;
     case KVD_OPT_COALESCE:
       p->coalesce = value ? 1 : 0;
       return KVD_OK;
     case KVD_OPT_VARIANT:
-      if (value < KVD_VARIANT_AUTO || value > KVD_VARIANT_CE)
+      if (value < KVD_VARIANT_AUTO || value > KVD_VARIANT_TMA)
         return fail(KVD_EINVAL, "variant %lld", (long long)value);
       p->variant = (int)value;
       return KVD_OK;
     case KVD_OPT_THREADS:
-      if (value < 128 || value > 1024 || value % 32)
-        return fail(KVD_EINVAL, "threads must be a multiple of 32 in [128, 1024]");
+      if (value < 32 || value > 1024 || value % 32)
+        return fail(KVD_EINVAL, "threads must be a multiple of 32 in [32, 1024]");
       p->threads = (uint32_t)value;
+      p->threads_set = true;
+      return KVD_OK;
+    case KVD_OPT_STAGES:
+      if (value < 2 || value > (int64_t)kvd::max_stages())
+        return fail(KVD_EINVAL, "stages must be in [2, %u]", kvd::max_stages());
+      p->stages = (uint32_t)value;
+      p->stages_set = true;
       return KVD_OK;
   }
   return fail(KVD_EINVAL, "unknown option %d", option);
@@ -788,26 +800,44 @@ kvd_status kvd_peer_set(kvd_peer p, int option, int64_t value) {
 // ===========================================================================
 // ABI: a3-a6 pull
 // ===========================================================================
-kvd_status kvd_pull(kvd_peer p, uint64_t request_id, const int32_t* src_ids,
-                    const int32_t* dst_ids, uint32_t n, void* stream_) {
+// Pull (push = false): remote (imported) cache -> local cache, kernel on the
+// local GPU reading over NVLink.  Push (push = true, §8 f2): local cache ->
+// remote cache, kernel on the local GPU storing over NVLink.
+static kvd_status transfer(kvd_peer p, uint64_t request_id, const int32_t* src_ids,
+                           const int32_t* dst_ids, uint32_t n, void* stream_, bool push) {
   if (!p) return fail(KVD_EINVAL, "null peer");
   std::lock_guard<std::mutex> lk(p->mu);
   if (p->closed) return fail(KVD_ESTATE, "peer closed");
   if (p->inflight.count(request_id))
     return fail(KVD_EBUSY, "request %llu already in flight", (unsigned long long)request_id);
-  const kvd_geometry& sg = p->remote.g;
-  const kvd_geometry& dg_ = p->local->geom.g;
+  const Geom& SG = push ? p->local->geom : p->remote;
+  const Geom& DG = push ? p->remote : p->local->geom;
+  const kvd_geometry& sg = SG.g;
+  const kvd_geometry& dg_ = DG.g;
+  const std::vector<uint64_t>& src_b = push ? p->local->bases : p->src_bases;
+  const std::vector<uint64_t>& dst_b = push ? p->src_bases : p->local->bases;
   // a3: validate + coalesce
-  kvd_status s = p->planner.plan(src_ids, dst_ids, n, p->remote.layout.num_blocks,
-                                 p->local->geom.layout.num_blocks, p->coalesce != 0, p->runs);
+  kvd_status s = p->planner.plan(src_ids, dst_ids, n, SG.layout.num_blocks, DG.layout.num_blocks,
+                                 p->coalesce != 0, p->runs);
   if (s != KVD_OK) return s;
   const PairPlan pp = pair_plan(sg, dg_);
   const uint32_t NL = p->local->geom.layout.num_layers;
   kvd::PullArgs a{};
-  a.src = kvd::SideAddr{p->d_src_bases, 0, 0, sg.plane_stride_bytes, sg.block_stride_bytes};
-  a.dst = kvd::SideAddr{p->local->d_bases, 0, 0, dg_.plane_stride_bytes, dg_.block_stride_bytes};
+  a.src = kvd::SideAddr{push ? p->local->d_bases : p->d_src_bases, 0, 0, sg.plane_stride_bytes,
+                        sg.block_stride_bytes};
+  a.dst = kvd::SideAddr{push ? p->d_src_bases : p->local->d_bases, 0, 0, dg_.plane_stride_bytes,
+                        dg_.block_stride_bytes};
+  // AUTO: over NVLink the TMA ring (1 pipe x 6 stages x 32 KiB per CTA, 32
+  // CTAs) saturates the link with ~22% of the SMs; in loopback (both caches
+  // on this GPU) the copy is HBM-bound and the full-grid LSU mover is used.
+  const bool over_link = p->remote_device != p->local->device;
+  const bool autov = p->variant == KVD_VARIANT_AUTO;
+  int variant = autov ? (over_link ? KVD_VARIANT_TMA : KVD_VARIANT_LSU) : p->variant;
+  const bool tma_defaults = variant == KVD_VARIANT_TMA && autov;
+  const uint32_t tile = (tma_defaults && !p->tile_set) ? 32768u : p->tile_bytes;
+  uint32_t stages = (tma_defaults && !p->stages_set) ? 6u : p->stages;
   if (n) {
-    s = tile_runs(p->runs, pp, NL, p->tile_bytes, p->runs4, a);
+    s = tile_runs(p->runs, pp, NL, tile, p->runs4, a);
     if (s != KVD_OK) return s;
   }
   // a6: completion slot
@@ -830,7 +860,6 @@ kvd_status kvd_pull(kvd_peer p, uint64_t request_id, const int32_t* src_ids,
   info.blocks = n;
   info.runs = (uint32_t)p->runs.size();
   info.bytes = (uint64_t)n * NL * 2 * sg.span_bytes;
-  int variant = p->variant == KVD_VARIANT_AUTO ? KVD_VARIANT_LSU : p->variant;
   cudaError_t e = cudaSuccess;
   if (n == 0) {
     e = kvd::launch_flag_only(a.flag, token, stream);
@@ -838,7 +867,6 @@ kvd_status kvd_pull(kvd_peer p, uint64_t request_id, const int32_t* src_ids,
     info.ctas = 1;
   } else if (variant == KVD_VARIANT_CE) {
     // copy-engine comparator: one cudaMemcpyAsync per contiguous segment
-    const std::vector<uint64_t>& src_b = p->src_bases;
     uint32_t launches = 0;
     for (uint32_t l = 0; l < NL && e == cudaSuccess; ++l)
       for (uint32_t pl = 0; pl < pp.planes && e == cudaSuccess; ++pl)
@@ -847,7 +875,7 @@ kvd_status kvd_pull(kvd_peer p, uint64_t request_id, const int32_t* src_ids,
           const uint64_t bytes = pp.contiguous ? (uint64_t)r.len * pp.unit : pp.unit;
           for (uint32_t j = 0; j < nb && e == cudaSuccess; ++j) {
             const uint64_t so = src_b[l] + pl * sg.plane_stride_bytes + (uint64_t)(r.src_start + j) * sg.block_stride_bytes;
-            const uint64_t d0 = p->local->bases[l] + pl * dg_.plane_stride_bytes + (uint64_t)(r.dst_start + j) * dg_.block_stride_bytes;
+            const uint64_t d0 = dst_b[l] + pl * dg_.plane_stride_bytes + (uint64_t)(r.dst_start + j) * dg_.block_stride_bytes;
             e = cudaMemcpyAsync((void*)(uintptr_t)d0, (const void*)(uintptr_t)so, bytes,
                                 cudaMemcpyDeviceToDevice, stream);
             ++launches;
@@ -857,7 +885,7 @@ kvd_status kvd_pull(kvd_peer p, uint64_t request_id, const int32_t* src_ids,
     info.launches = launches + 1;
     info.segments = launches;
   } else {
-    if (variant == KVD_VARIANT_LSU32 && !aligned32(a, p->src_bases, p->local->bases))
+    if (variant == KVD_VARIANT_LSU32 && !aligned32(a, src_b, dst_b))
       variant = KVD_VARIANT_LSU;
     // big run tables go through a per-slot device buffer
     if (a.nruns > kvd::max_param_runs()) {
@@ -877,16 +905,35 @@ kvd_status kvd_pull(kvd_peer p, uint64_t request_id, const int32_t* src_ids,
       a.runs_dev = p->slot_runs_dev[slot];
       info.launches = 1;   // the H2D copy (not a kernel)
     }
+    const uint32_t threads =
+        p->threads_set ? p->threads : (variant == KVD_VARIANT_TMA ? (tma_defaults ? 32u : 96u) : 512u);
+    if (variant == KVD_VARIANT_TMA) {
+      uint64_t smem = (uint64_t)(threads / 32) * stages * a.tile_bytes;
+      if (tma_defaults && !p->stages_set && smem > 225u * 1024u) {   // auto: shrink the ring
+        stages = (uint32_t)std::max<uint64_t>(2, (225u * 1024u) / ((threads / 32) * (uint64_t)a.tile_bytes));
+        smem = (uint64_t)(threads / 32) * stages * a.tile_bytes;
+      }
+      if (smem > 225u * 1024u)   // 227 KiB per CTA minus the 2 KiB mbarrier array
+        return fail(KVD_EINVAL, "TMA ring needs %llu B of shared memory (pipes %u x stages %u x "
+                    "tile %u); max 225 KiB", (unsigned long long)smem, threads / 32, stages,
+                    a.tile_bytes);
+    } else if (threads < 128) {
+      return fail(KVD_EINVAL, "LSU variants need >= 128 threads per CTA");
+    }
     uint32_t max_ctas = p->max_ctas;
     if (!max_ctas) {
-      const int per_sm = kvd::pull_ctas_per_sm(variant, p->threads, a.nruns);
-      max_ctas = (uint32_t)(p->sm_count * per_sm);
+      if (tma_defaults) {
+        max_ctas = 32;
+      } else {
+        const int per_sm = kvd::pull_ctas_per_sm(variant, threads, a.nruns);
+        max_ctas = (uint32_t)(p->sm_count * per_sm);
+      }
     }
-    const uint32_t ctas = grid_for(a.total_tiles, p->threads, max_ctas);
-    e = kvd::launch_pull(a, p->runs4.data(), variant, ctas, p->threads, stream);
+    const uint32_t ctas = grid_for(a.total_tiles, threads, max_ctas);
+    e = kvd::launch_pull(a, p->runs4.data(), variant, ctas, threads, stages, stream);
     info.launches += 1;
     info.ctas = ctas;
-    info.threads = p->threads;
+    info.threads = threads;
     info.tiles = a.total_tiles;
     info.segments = (uint64_t)NL * pp.planes * (pp.contiguous ? p->runs.size() : n);
   }
@@ -897,6 +944,16 @@ kvd_status kvd_pull(kvd_peer p, uint64_t request_id, const int32_t* src_ids,
   p->inflight[request_id] = std::make_pair(slot, token);
   p->last = info;
   return KVD_OK;
+}
+
+kvd_status kvd_pull(kvd_peer p, uint64_t request_id, const int32_t* src_ids,
+                    const int32_t* dst_ids, uint32_t n, void* stream) {
+  return transfer(p, request_id, src_ids, dst_ids, n, stream, false);
+}
+
+kvd_status kvd_push(kvd_peer p, uint64_t request_id, const int32_t* src_ids,
+                    const int32_t* dst_ids, uint32_t n, void* stream) {
+  return transfer(p, request_id, src_ids, dst_ids, n, stream, true);
 }
 
 kvd_status kvd_poll_done(kvd_peer p, uint64_t request_id, int* done) {
@@ -984,7 +1041,7 @@ static kvd_status gather_scatter(kvd_cache c, const int32_t* ids, uint32_t n, ui
   const uint32_t threads = 512;
   const uint32_t ctas = grid_for(a.total_tiles, threads,
                                  (uint32_t)(dev_sms * kvd::pull_ctas_per_sm(KVD_VARIANT_LSU, threads, a.nruns)));
-  cudaError_t e = kvd::launch_pull(a, c->runs4.data(), KVD_VARIANT_LSU, ctas, threads,
+  cudaError_t e = kvd::launch_pull(a, c->runs4.data(), KVD_VARIANT_LSU, ctas, threads, 0,
                                    (cudaStream_t)stream_);
   if (e != cudaSuccess) return cuda_fail(e, gather ? "gather launch" : "scatter launch");
   return KVD_OK;

@@ -42,15 +42,20 @@ struct PullArgs {
   const int4* runs_dev;             // run table in device memory when nruns > params capacity
 };
 
-enum Variant : int { kLsu16 = 1, kLsu32 = 2 };
+enum Variant : int { kLsu16 = 1, kLsu32 = 2, kTma = 4 };
 
 // Largest run table that travels inside the kernel parameters.
 unsigned int max_param_runs();
+// Deepest TMA ring (stages per pipe).
+unsigned int max_stages();
 
 // Launch one pull kernel.  runs_host must hold args.nruns entries when
 // args.nruns <= max_param_runs(); otherwise args.runs_dev is used.
+// variant kTma: threads/32 pipes per CTA, each an S-stage ring of tile_bytes
+// buffers in dynamic shared memory (stages in [2, max_stages()]).
 cudaError_t launch_pull(const PullArgs& args, const int4* runs_host, int variant,
-                        unsigned int ctas, unsigned int threads, cudaStream_t stream);
+                        unsigned int ctas, unsigned int threads, unsigned int stages,
+                        cudaStream_t stream);
 
 // Completion with no bytes (n = 0, or after copy-engine copies).
 cudaError_t launch_flag_only(unsigned long long* flag, unsigned long long token,

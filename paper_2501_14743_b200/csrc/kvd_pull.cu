@@ -1,18 +1,26 @@
-// kvd_pull.cu -- the sm_100a pull kernel and its
+// kvd_pull.cu -- the sm_100a pull kernels and their
 // completion epilogue (row a6).
 //
 // PAPER.md §4.3: in pull mode the decode worker "reads the blocks
 // from the prefill worker" and "performs KV cache reads for all layers in a
-// single shot".  Here the reads are one-sided SM loads from the prefill
-// GPU's HBM, mapped into this process with CUDA IPC, over NVLink 5 /
-// NVSwitch; the writes are local HBM stores into the decode cache's blocks.
-// One launch covers every layer, both K and V, and every coalesced run
-// (P:L377-378); the last CTA to finish raises the request's completion word
-// ("The completion transaction sends the request ID"), so the host
-// never synchronises per block.
+// single shot".  Here the reads are one-sided loads from the prefill GPU's
+// HBM, mapped into this process with CUDA IPC, over NVLink 5 / NVSwitch; the
+// writes are local HBM stores into the decode cache's blocks.  One launch
+// covers every layer, both K and V, and every coalesced run; the
+// last CTA to finish raises the request's completion word ("The
+// completion transaction sends the request ID"), so the host never
+// synchronises per block.
 //
-// The copy is a bit copy through integer vector registers only (no float
-// type ever touches the data), so NaN payloads, -0 and subnormals survive.
+// Two data movers share the tiling and the epilogue:
+//   * LSU  -- every warp copies whole tiles with 16 B (or 32 B) vector
+//             loads/stores through registers, 8 loads in flight per lane.
+//   * TMA  -- one elected lane per warp ("pipe") runs an S-stage ring of
+//             cp.async.bulk copies: peer HBM -> shared memory (mbarrier
+//             complete_tx), then shared memory -> local HBM (bulk group).
+//             Up to ~200 KiB per SM in flight without registers, so far
+//             fewer SMs saturate NVLink and the rest stay free for decode.
+// Both are bit copies through integer registers / shared memory only (no
+// float type ever touches the data): NaN payloads, -0, subnormals survive.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -26,6 +34,7 @@ namespace {
 constexpr int kRunsSmall = 64;
 constexpr int kRunsMid = 512;
 constexpr int kRunsLarge = 2016;
+constexpr int kMaxStages = 8;
 
 template <int MAXR>
 struct PullParams {
@@ -69,7 +78,7 @@ __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned l
 
 // One warp copies `bytes` (multiple of sizeof(V)) from src to dst.  All U
 // loads of a batch are issued before any store so each lane keeps U
-// independent NVLink reads in flight (Little's law, DESIGN.md §Kernels).
+// independent NVLink reads in flight (Little's law, DESIGN.md §6).
 template <typename V, int U>
 __device__ __forceinline__ void warp_copy(char* __restrict__ dst, const char* __restrict__ src,
                                           unsigned int bytes, unsigned int lane) {
@@ -91,58 +100,50 @@ __device__ __forceinline__ unsigned long long layer_base(const SideAddr& s, unsi
   return s.table ? s.table[l] : s.base + (unsigned long long)l * s.step;
 }
 
-template <int MAXR, typename V, int U>
-__global__ void __launch_bounds__(1024)
-pull_kernel(const __grid_constant__ PullParams<MAXR> P) {
-  const PullArgs& a = P.a;
-  const int4* runs = (MAXR > 0) ? P.runs : a.runs_dev;
-  const unsigned int lane = threadIdx.x & 31u;
-  const unsigned int warps_per_cta = blockDim.x >> 5;
-  const unsigned int nwarps = gridDim.x * warps_per_cta;
-
-  for (unsigned int t = blockIdx.x * warps_per_cta + (threadIdx.x >> 5); t < a.total_tiles;
-       t += nwarps) {
-    // tile -> (layer, plane, run, offset); all warp-uniform
-    const unsigned int lp = t / a.tiles_per_lp;
-    const unsigned int k = t - lp * a.tiles_per_lp;
-    const unsigned int l = (a.planes == 2) ? (lp >> 1) : lp;
-    const unsigned int p = (a.planes == 2) ? (lp & 1u) : 0u;
-    int lo = 0, hi = (int)a.nruns - 1;                 // first run with tile_end > k
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if ((unsigned int)runs[mid].w > k) hi = mid; else lo = mid + 1;
-    }
-    const int4 run = runs[lo];
-    const unsigned int kr = k - (lo ? (unsigned int)runs[lo - 1].w : 0u);
-
-    unsigned long long src_off, dst_off, off, avail;
-    if (a.contiguous) {
-      off = (unsigned long long)kr * a.tile_bytes;
-      avail = (unsigned long long)(unsigned int)run.z * a.unit_bytes - off;
-      src_off = (unsigned long long)run.x * a.src.block_stride + off;
-      dst_off = (unsigned long long)run.y * a.dst.block_stride + off;
-    } else {
-      const unsigned int j = kr / a.tiles_per_unit;
-      const unsigned int kk = kr - j * a.tiles_per_unit;
-      off = (unsigned long long)kk * a.tile_bytes;
-      avail = a.unit_bytes - off;
-      src_off = (unsigned long long)(run.x + (int)j) * a.src.block_stride + off;
-      dst_off = (unsigned long long)(run.y + (int)j) * a.dst.block_stride + off;
-    }
-    const unsigned int bytes = avail < a.tile_bytes ? (unsigned int)avail : a.tile_bytes;
-    const char* src = reinterpret_cast<const char*>(
-        layer_base(a.src, l) + (unsigned long long)p * a.src.plane_stride + src_off);
-    char* dst = reinterpret_cast<char*>(
-        layer_base(a.dst, l) + (unsigned long long)p * a.dst.plane_stride + dst_off);
-    warp_copy<V, U>(dst, src, bytes, lane);
+// Tile t -> (source address, destination address, bytes).  Segments are
+// (layer, plane, run); a tile never crosses one.  runs[r].w is the inclusive
+// tile prefix over runs within one (layer, plane).
+__device__ __forceinline__ unsigned int tile_addr(const PullArgs& a, const int4* runs,
+                                                  unsigned int t, const char*& src, char*& dst) {
+  const unsigned int lp = t / a.tiles_per_lp;
+  const unsigned int k = t - lp * a.tiles_per_lp;
+  const unsigned int l = (a.planes == 2) ? (lp >> 1) : lp;
+  const unsigned int p = (a.planes == 2) ? (lp & 1u) : 0u;
+  int lo = 0, hi = (int)a.nruns - 1;                 // first run with tile_end > k
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if ((unsigned int)runs[mid].w > k) hi = mid; else lo = mid + 1;
   }
+  const int4 run = runs[lo];
+  const unsigned int kr = k - (lo ? (unsigned int)runs[lo - 1].w : 0u);
+  unsigned long long src_off, dst_off, off, avail;
+  if (a.contiguous) {
+    off = (unsigned long long)kr * a.tile_bytes;
+    avail = (unsigned long long)(unsigned int)run.z * a.unit_bytes - off;
+    src_off = (unsigned long long)run.x * a.src.block_stride + off;
+    dst_off = (unsigned long long)run.y * a.dst.block_stride + off;
+  } else {
+    const unsigned int j = kr / a.tiles_per_unit;
+    const unsigned int kk = kr - j * a.tiles_per_unit;
+    off = (unsigned long long)kk * a.tile_bytes;
+    avail = a.unit_bytes - off;
+    src_off = (unsigned long long)(run.x + (int)j) * a.src.block_stride + off;
+    dst_off = (unsigned long long)(run.y + (int)j) * a.dst.block_stride + off;
+  }
+  src = reinterpret_cast<const char*>(layer_base(a.src, l) +
+                                      (unsigned long long)p * a.src.plane_stride + src_off);
+  dst = reinterpret_cast<char*>(layer_base(a.dst, l) +
+                                (unsigned long long)p * a.dst.plane_stride + dst_off);
+  return avail < a.tile_bytes ? (unsigned int)avail : a.tile_bytes;
+}
 
-  // Completion (row a6): every thread orders its stores at gpu scope, the
-  // CTA arrives once; the last CTA resets the slot counter and publishes the
-  // token with a system-scope release so a host acquire load of the flag
-  // implies every byte of the request is visible.
+// Completion (row a6): every thread orders its stores at system scope (in
+// push mode they went to a peer GPU), the CTA arrives once; the last CTA
+// resets the slot counter and publishes the token with a system-scope
+// release, so a host acquire load of the word implies every byte landed.
+__device__ __forceinline__ void complete(const PullArgs& a) {
   if (a.counter == nullptr) return;   // baseline gather/scatter: stream order only
-  __threadfence();
+  __threadfence_system();
   __syncthreads();
   if (threadIdx.x == 0) {
     const unsigned int prev = atomicAdd(a.counter, 1u);
@@ -154,19 +155,153 @@ pull_kernel(const __grid_constant__ PullParams<MAXR> P) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// LSU mover: one warp per tile
+// ---------------------------------------------------------------------------
+template <int MAXR, typename V, int U>
+__global__ void __launch_bounds__(1024)
+pull_kernel(const __grid_constant__ PullParams<MAXR> P) {
+  const PullArgs& a = P.a;
+  const int4* runs = (MAXR > 0) ? P.runs : a.runs_dev;
+  const unsigned int lane = threadIdx.x & 31u;
+  const unsigned int warps_per_cta = blockDim.x >> 5;
+  const unsigned int nwarps = gridDim.x * warps_per_cta;
+  for (unsigned int t = blockIdx.x * warps_per_cta + (threadIdx.x >> 5); t < a.total_tiles;
+       t += nwarps) {
+    const char* src;
+    char* dst;
+    const unsigned int bytes = tile_addr(a, runs, t, src, dst);
+    warp_copy<V, U>(dst, src, bytes, lane);
+  }
+  complete(a);
+}
+
+// ---------------------------------------------------------------------------
+// TMA mover: one elected lane per warp runs an S-stage bulk-copy ring
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tma_load(void* smem, const void* gsrc, unsigned int bytes,
+                                         uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+               :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      :: "r"(smem_u32(smem)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" :: "r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_store(void* gdst, const void* smem, unsigned int bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+               :: "l"(gdst), "r"(smem_u32(smem)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void tma_wait_read_1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+__device__ __forceinline__ void tma_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+template <int MAXR>
+__global__ void __launch_bounds__(1024)
+pull_kernel_tma(const __grid_constant__ PullParams<MAXR> P, unsigned int stages) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ uint64_t bars[32 * kMaxStages];
+  const PullArgs& a = P.a;
+  const int4* runs = (MAXR > 0) ? P.runs : a.runs_dev;
+  const unsigned int warp = threadIdx.x >> 5;
+  const unsigned int pipes_per_cta = blockDim.x >> 5;
+  const unsigned int npipes = gridDim.x * pipes_per_cta;
+  const unsigned int pipe = blockIdx.x * pipes_per_cta + warp;
+  const unsigned int S = stages;
+  unsigned char* ring = smem + (size_t)warp * S * a.tile_bytes;
+  uint64_t* bar = bars + warp * kMaxStages;
+
+  if ((threadIdx.x & 31u) == 0) {
+    for (unsigned int s = 0; s < S; ++s) mbar_init(&bar[s]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+
+    // tile i of this pipe = pipe + i * npipes
+    const unsigned int count =
+        pipe < a.total_tiles ? (a.total_tiles - pipe + npipes - 1) / npipes : 0u;
+    char* dsts[kMaxStages];
+    unsigned int sizes[kMaxStages];
+    for (unsigned int k = 0; k < S && k < count; ++k) {
+      const char* src;
+      sizes[k] = tile_addr(a, runs, pipe + k * npipes, src, dsts[k]);
+      tma_load(ring + (size_t)k * a.tile_bytes, src, sizes[k], &bar[k]);
+    }
+    for (unsigned int i = 0; i < count; ++i) {
+      const unsigned int s = i % S;
+      mbar_wait(&bar[s], (i / S) & 1u);
+      tma_store(dsts[s], ring + (size_t)s * a.tile_bytes, sizes[s]);
+      if (i >= 1) {
+        // store i-1 has finished reading its stage: refill it with tile i-1+S
+        tma_wait_read_1();
+        const unsigned int k = i - 1 + S;
+        if (k < count) {
+          const unsigned int sk = k % S;
+          const char* src;
+          sizes[sk] = tile_addr(a, runs, pipe + k * npipes, src, dsts[sk]);
+          tma_load(ring + (size_t)sk * a.tile_bytes, src, sizes[sk], &bar[sk]);
+        }
+      }
+    }
+    tma_wait_all();
+  }
+  __syncwarp();
+  complete(a);
+}
+
 __global__ void flag_kernel(unsigned long long* flag, unsigned long long token) {
   __threadfence_system();
   st_release_sys(flag, token);
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+template <int MAXR>
+void fill(PullParams<MAXR>& P, const PullArgs& args, const int4* runs_host) {
+  P.a = args;
+  if (MAXR > 0)
+    for (unsigned int r = 0; r < args.nruns; ++r) P.runs[r] = runs_host[r];
 }
 
 template <int MAXR, typename V, int U>
 cudaError_t launch_t(const PullArgs& args, const int4* runs_host, unsigned int ctas,
                      unsigned int threads, cudaStream_t stream) {
   PullParams<MAXR> P;
-  P.a = args;
-  if (MAXR > 0)
-    for (unsigned int r = 0; r < args.nruns; ++r) P.runs[r] = runs_host[r];
+  fill(P, args, runs_host);
   pull_kernel<MAXR, V, U><<<ctas, threads, 0, stream>>>(P);
+  return cudaGetLastError();
+}
+
+template <int MAXR>
+cudaError_t launch_tma_t(const PullArgs& args, const int4* runs_host, unsigned int ctas,
+                         unsigned int threads, unsigned int stages, cudaStream_t stream) {
+  PullParams<MAXR> P;
+  fill(P, args, runs_host);
+  const size_t smem = (size_t)(threads / 32) * stages * args.tile_bytes;
+  // per function and device (the static mbarrier array counts against the
+  // 48 KiB default too); cheap, so set on every launch
+  cudaError_t e = cudaFuncSetAttribute(pull_kernel_tma<MAXR>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  pull_kernel_tma<MAXR><<<ctas, threads, smem, stream>>>(P, stages);
   return cudaGetLastError();
 }
 
@@ -182,6 +317,17 @@ cudaError_t launch_v(const PullArgs& args, const int4* runs_host, unsigned int c
   return launch_t<0, V, U>(args, runs_host, ctas, threads, stream);
 }
 
+cudaError_t launch_tma(const PullArgs& args, const int4* runs_host, unsigned int ctas,
+                       unsigned int threads, unsigned int stages, cudaStream_t stream) {
+  if (args.nruns <= (unsigned)kRunsSmall)
+    return launch_tma_t<kRunsSmall>(args, runs_host, ctas, threads, stages, stream);
+  if (args.nruns <= (unsigned)kRunsMid)
+    return launch_tma_t<kRunsMid>(args, runs_host, ctas, threads, stages, stream);
+  if (args.nruns <= (unsigned)kRunsLarge)
+    return launch_tma_t<kRunsLarge>(args, runs_host, ctas, threads, stages, stream);
+  return launch_tma_t<0>(args, runs_host, ctas, threads, stages, stream);
+}
+
 template <int MAXR, typename V, int U>
 int occ(unsigned int threads) {
   int n = 0;
@@ -194,9 +340,12 @@ int occ(unsigned int threads) {
 }  // namespace
 
 unsigned int max_param_runs() { return (unsigned int)kRunsLarge; }
+unsigned int max_stages() { return (unsigned int)kMaxStages; }
 
 cudaError_t launch_pull(const PullArgs& args, const int4* runs_host, int variant,
-                        unsigned int ctas, unsigned int threads, cudaStream_t stream) {
+                        unsigned int ctas, unsigned int threads, unsigned int stages,
+                        cudaStream_t stream) {
+  if (variant == kTma) return launch_tma(args, runs_host, ctas, threads, stages, stream);
   if (variant == kLsu32) return launch_v<V32, 4>(args, runs_host, ctas, threads, stream);
   return launch_v<V16, 8>(args, runs_host, ctas, threads, stream);
 }
@@ -208,6 +357,7 @@ cudaError_t launch_flag_only(unsigned long long* flag, unsigned long long token,
 }
 
 int pull_ctas_per_sm(int variant, unsigned int threads, unsigned int nruns) {
+  if (variant == kTma) return 1;   // shared-memory ring sized for one CTA per SM
   const bool big = nruns > (unsigned)kRunsLarge;
   if (variant == kLsu32) return big ? occ<0, V32, 4>(threads) : occ<kRunsSmall, V32, 4>(threads);
   return big ? occ<0, V16, 8>(threads) : occ<kRunsSmall, V16, 8>(threads);

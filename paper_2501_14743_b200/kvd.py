@@ -18,13 +18,13 @@ LIB_PATH = os.path.join(_HERE, "libkvd.so")
 
 OK, EINVAL, ERANGE, ELAYOUT, EHANDLE, ECUDA, ENOMEM, EBUSY, ESTATE = 0, -1, -2, -3, -4, -5, -6, -7, -8
 FP16, BF16, FP8, FP32 = 0, 1, 2, 3
-VARIANT_AUTO, VARIANT_LSU, VARIANT_LSU32, VARIANT_CE = 0, 1, 2, 3
-OPT_MAX_CTAS, OPT_TILE_BYTES, OPT_COALESCE, OPT_VARIANT, OPT_THREADS = 0, 1, 2, 3, 4
+VARIANT_AUTO, VARIANT_LSU, VARIANT_LSU32, VARIANT_CE, VARIANT_TMA = 0, 1, 2, 3, 4
+OPT_MAX_CTAS, OPT_TILE_BYTES, OPT_COALESCE, OPT_VARIANT, OPT_THREADS, OPT_STAGES = 0, 1, 2, 3, 4, 5
 
 EXPORTED = (
     "kvd_layout_geometry", "kvd_plan", "kvd_blob_info", "kvd_register_cache",
     "kvd_unregister_cache", "kvd_export_handle", "kvd_open_peer", "kvd_close_peer",
-    "kvd_peer_set", "kvd_pull", "kvd_poll_done", "kvd_wait_done", "kvd_last_pull_info",
+    "kvd_peer_set", "kvd_pull", "kvd_push", "kvd_poll_done", "kvd_wait_done", "kvd_last_pull_info",
     "kvd_gather", "kvd_scatter", "kvd_strerror", "kvd_last_error", "kvd_abi_version",
 )
 
@@ -89,6 +89,7 @@ _SIGS = {
     "kvd_close_peer": [_p],
     "kvd_peer_set": [_p, ctypes.c_int, _i64],
     "kvd_pull": [_p, _u64, _pi32, _pi32, _u32, _p],
+    "kvd_push": [_p, _u64, _pi32, _pi32, _u32, _p],
     "kvd_poll_done": [_p, _u64, ctypes.POINTER(ctypes.c_int)],
     "kvd_wait_done": [_p, _u64, _i64],
     "kvd_last_pull_info": [_p, ctypes.POINTER(kvd_pull_info)],
@@ -217,6 +218,15 @@ def kvd_pull(peer: int, request_id: int, src_ids, dst_ids, stream: Optional[int]
         raise ValueError("src_ids and dst_ids differ in length")
     _check(_lib.kvd_pull(peer, request_id, _ptr_i32(s), _ptr_i32(d), s.size, stream or None),
            "kvd_pull")
+
+
+def kvd_push(peer: int, request_id: int, src_ids, dst_ids, stream: Optional[int] = None) -> None:
+    """Push variant: local blocks src_ids -> remote blocks dst_ids (launch on the local GPU)."""
+    s, d = _ids(src_ids), _ids(dst_ids)
+    if s.size != d.size:
+        raise ValueError("src_ids and dst_ids differ in length")
+    _check(_lib.kvd_push(peer, request_id, _ptr_i32(s), _ptr_i32(d), s.size, stream or None),
+           "kvd_push")
 
 
 def kvd_poll_done(peer: int, request_id: int) -> bool:

@@ -81,6 +81,11 @@ class Peer:
         s = stream if stream is not None else torch.cuda.current_stream(self.local.device)
         kvd.kvd_pull(self.handle, request_id, src_ids, dst_ids, s.cuda_stream)
 
+    def push(self, request_id: int, src_ids, dst_ids, stream: Optional[torch.cuda.Stream] = None):
+        """§8 f2: local blocks -> the imported cache's blocks (stores over NVLink)."""
+        s = stream if stream is not None else torch.cuda.current_stream(self.local.device)
+        kvd.kvd_push(self.handle, request_id, src_ids, dst_ids, s.cuda_stream)
+
     def poll(self, request_id: int) -> bool:
         return kvd.kvd_poll_done(self.handle, request_id)
 

@@ -89,13 +89,16 @@ def test_geometries_bit_exact(geom):
         pair.close()
 
 
-@pytest.mark.parametrize("variant", [kvd.VARIANT_LSU, kvd.VARIANT_LSU32, kvd.VARIANT_CE])
+@pytest.mark.parametrize("variant", [kvd.VARIANT_LSU, kvd.VARIANT_LSU32, kvd.VARIANT_CE,
+                                     kvd.VARIANT_TMA])
 @pytest.mark.parametrize("tile", [512, 4096, 16384, 65536])
 def test_variants_and_tiles(variant, tile):
     g = kvdgen.CacheGeom(4, 4, 64, 16, 96, kvdgen.FP16)   # 8 KiB spans
     pair = make_pair(g, g, seed=4)
     try:
         pair.peer.set(kvd.OPT_VARIANT, variant).set(kvd.OPT_TILE_BYTES, tile)
+        if variant == kvd.VARIANT_TMA and tile == 65536:
+            pair.peer.set(kvd.OPT_THREADS, 32).set(kvd.OPT_STAGES, 3)   # fit 227 KiB
         src, dst = kvdgen.fragmented_table(60, 96, 96, seed=tile)
         info = pull_and_wait(pair, src, dst)
         assert info["variant"] == variant
@@ -345,4 +348,86 @@ def test_two_gpus_same_process():
             assert_layers_equal(pair.download_dst(), pair.expected(src, dst, pre))
     finally:
         torch.cuda.set_device(0)
+        pair.close()
+
+
+@pytest.mark.parametrize("kind", ["contiguous", "fragmented", "random"])
+def test_push_variant_bit_exact(kind):
+    """§8 f2: the push variant (kernel on the prefill side storing into the
+    imported decode cache) gives the oracle's result too."""
+    pair = make_pair(C1, C1, seed=16)
+    try:
+        # open the reverse binding: local = prefill cache, imported = decode cache
+        rev = pair.src.open_peer(pair.dst.export())
+        src, dst = _tables(kind, N_C1, 64, 64, seed=6)
+        rid = next_request_id()
+        rev.push(rid, src, dst)
+        rev.wait(rid)
+        assert rev.info()["bytes"] == N_C1 * 2 * 2 * 4096
+        assert_layers_equal(pair.download_dst(), pair.expected(src, dst))
+        rev.close()
+    finally:
+        pair.close()
+
+
+@pytest.mark.gpu2
+def test_push_two_gpus():
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs")
+    g = kvdgen.CacheGeom(4, 8, 128, 16, 300, kvdgen.FP16)
+    pair = make_pair(g, g, seed=17, src_dev=0, dst_dev=1)
+    try:
+        rev = pair.src.open_peer(pair.dst.export())
+        src, dst = kvdgen.fragmented_table(200, 300, 300, seed=2)
+        rid = next_request_id()
+        rev.push(rid, src, dst)
+        rev.wait(rid)
+        assert_layers_equal(pair.download_dst(), pair.expected(src, dst))
+        rev.close()
+    finally:
+        pair.close()
+
+
+@pytest.mark.parametrize("threads,stages,ctas", [(32, 2, 1), (96, 4, 0), (256, 2, 5), (64, 8, 3)])
+@pytest.mark.parametrize("kind", ["fragmented", "random", "contiguous"])
+def test_tma_ring_shapes(threads, stages, ctas, kind):
+    """TMA mover: ring depth, pipes per CTA and grid size never change the
+    bytes (ragged tiles, more tiles than pipes, fewer tiles than pipes)."""
+    g = kvdgen.CacheGeom(3, 4, 64, 16, 128, kvdgen.FP16)
+    pair = make_pair(g, g, seed=18)
+    try:
+        pair.peer.set(kvd.OPT_VARIANT, kvd.VARIANT_TMA).set(kvd.OPT_THREADS, threads)
+        pair.peer.set(kvd.OPT_STAGES, stages).set(kvd.OPT_MAX_CTAS, ctas)
+        pair.peer.set(kvd.OPT_TILE_BYTES, 3072)
+        src, dst = _tables(kind, 77, 128, 128, seed=threads)
+        info = pull_and_wait(pair, src, dst)
+        assert info["variant"] == kvd.VARIANT_TMA
+        assert_layers_equal(pair.download_dst(), pair.expected(src, dst))
+    finally:
+        pair.close()
+
+
+def test_tma_rejects_oversized_ring():
+    pair = make_pair(C1, C1, seed=19)
+    try:
+        pair.peer.set(kvd.OPT_VARIANT, kvd.VARIANT_TMA).set(kvd.OPT_THREADS, 1024)
+        with pytest.raises(kvd.KvdError) as ei:
+            pair.peer.pull(next_request_id(), [0], [1])
+        assert ei.value.status == kvd.EINVAL
+    finally:
+        pair.close()
+
+
+@pytest.mark.gpu2
+def test_tma_two_gpus_c4_shard():
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs")
+    g = kvdgen.C4.with_blocks(600)
+    pair = make_pair(g, g, seed=20, src_dev=0, dst_dev=1)
+    try:
+        pair.peer.set(kvd.OPT_VARIANT, kvd.VARIANT_TMA)
+        src, dst = kvdgen.fragmented_table(512, 600, 600, seed=4)
+        pull_and_wait(pair, src, dst)
+        assert_layers_equal(pair.download_dst(), pair.expected(src, dst))
+    finally:
         pair.close()

@@ -25,7 +25,7 @@ import kvdgen
 from paper_2501_14743_b200 import kvd
 from paper_2501_14743_b200.torch_cache import PagedCache
 
-VAR = {"lsu": 1, "lsu32": 2, "ce": 3}
+VAR = {"lsu": 1, "lsu32": 2, "ce": 3, "tma": 4}
 
 
 def geom_of(name):
@@ -52,9 +52,11 @@ def main():
     ap.add_argument("--tiles", default="16384")
     ap.add_argument("--threads", default="512")
     ap.add_argument("--ctas", default="0")
+    ap.add_argument("--stages", default="4")
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--ce-ceiling", action="store_true")
+    ap.add_argument("--mode", choices=["pull", "push"], default="pull")
     ap.add_argument("--profile-once", action="store_true",
                     help="one warm-up pull then exactly one pull (for ncu -s/-c)")
     a = ap.parse_args()
@@ -69,14 +71,20 @@ def main():
         kvdgen.torch_fill_random_(dst.layers[l], 20 + l)
     torch.cuda.synchronize(a.src_dev)
     torch.cuda.synchronize(a.dst_dev)
-    peer = dst.open_peer(src.export())
-    torch.cuda.set_device(a.dst_dev)
-    stream = torch.cuda.Stream(a.dst_dev)
+    if a.mode == "push":     # kernel on the prefill GPU, stores over NVLink
+        peer = src.open_peer(dst.export())
+        run_dev = a.src_dev
+    else:
+        peer = dst.open_peer(src.export())
+        run_dev = a.dst_dev
+    torch.cuda.set_device(run_dev)
+    stream = torch.cuda.Stream(run_dev)
+    go = peer.push if a.mode == "push" else peer.pull
     rid = [0]
 
     def pull(s, d):
         rid[0] += 1
-        peer.pull(rid[0], s, d, stream)
+        go(rid[0], s, d, stream)
         peer.wait(rid[0])
 
     if a.profile_once:
@@ -109,12 +117,15 @@ def main():
                           "bytes": nbytes, "src": a.src_dev, "dst": a.dst_dev}), flush=True)
         del x, y
 
-    for kind, var, tile, thr, ctas in itertools.product(
+    for kind, var, tile, thr, ctas, st in itertools.product(
             a.tables.split(","), a.variants.split(","), [int(t) for t in a.tiles.split(",")],
-            [int(t) for t in a.threads.split(",")], [int(c) for c in a.ctas.split(",")]):
+            [int(t) for t in a.threads.split(",")], [int(c) for c in a.ctas.split(",")],
+            [int(x) for x in a.stages.split(",")]):
         s, d = tables(g, kind, n)
+        if var == "tma" and (thr // 32) * st * tile > 225 * 1024:
+            continue
         peer.set(kvd.OPT_VARIANT, VAR[var]).set(kvd.OPT_TILE_BYTES, tile)
-        peer.set(kvd.OPT_THREADS, thr).set(kvd.OPT_MAX_CTAS, ctas)
+        peer.set(kvd.OPT_THREADS, thr).set(kvd.OPT_MAX_CTAS, ctas).set(kvd.OPT_STAGES, st)
         for _ in range(a.warmup):
             pull(s, d)
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -124,15 +135,15 @@ def main():
             ev[k][0].record(stream)
             rid[0] += 1
             t0 = time.perf_counter()
-            peer.pull(rid[0], s, d, stream)
+            go(rid[0], s, d, stream)
             ev[k][1].record(stream)
             peer.wait(rid[0])
             lat.append(time.perf_counter() - t0)
         torch.cuda.synchronize()
         ms = [x.elapsed_time(y) for x, y in ev]
         info = peer.info()
-        print(json.dumps({"config": a.config, "table": kind, "variant": var, "tile": tile,
-                          "threads": thr, "ctas": info["ctas"], "runs": info["runs"],
+        print(json.dumps({"mode": a.mode, "config": a.config, "table": kind, "variant": var, "tile": tile,
+                          "threads": thr, "stages": st, "ctas": info["ctas"], "runs": info["runs"],
                           "kernel_ms_med": round(float(np.median(ms)), 4),
                           "gbs": round(info["bytes"] / (np.median(ms) / 1e3) / 1e9, 1),
                           "p50_lat_ms": round(float(np.median(lat)) * 1e3, 4)}), flush=True)
