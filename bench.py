@@ -343,14 +343,11 @@ def run_kvd(args, rank, world, local_rank):
     dev = local_rank
     g, tokens, s_ids, d_ids, desc = workload(args.config, args.table)
     n = len(s_ids)
+    from paper_2501_14743_b200 import cluster
     multi = world > 1
-    if multi:
-        half = world // 2
-        role = "prefill" if rank < half else "decode"
-        pairs = half
-        gloo = dist.new_group(backend="gloo")
-    else:
-        role, pairs, gloo = "both", 1, None
+    me = cluster.role_of(rank, world)
+    role, pairs, half = me.role, me.pairs, world // 2
+    gloo = dist.new_group(backend="gloo") if multi else None
 
     def new_cache(seed):
         c = PagedCache(g.num_layers, g.num_kv_heads, g.head_dim, g.block_size, g.num_blocks,
@@ -365,15 +362,15 @@ def run_kvd(args, rank, world, local_rank):
 
     # row a2: one-time tensor-centric exchange (Connect())
     if multi:
-        blobs = [None] * world
-        dist.all_gather_object(blobs, src.export() if src else None, group=gloo)
-        peer_blob = blobs[rank - half] if role == "decode" else None
+        blob = cluster.peer_blob(me, cluster.exchange_blobs(src.export() if src else None, gloo))
     else:
-        peer_blob = src.export()
-    peer = dst.open_peer(peer_blob) if dst else None
+        blob = src.export()
+    peer = dst.open_peer(blob) if dst else None
     if peer:
         if args.variant:
-            peer.set(kvd.OPT_VARIANT, {"lsu": 1, "lsu32": 2, "ce": 3}[args.variant])
+            peer.set(kvd.OPT_VARIANT, {"lsu": 1, "lsu32": 2, "ce": 3, "tma": 4}[args.variant])
+        if args.stages:
+            peer.set(kvd.OPT_STAGES, args.stages)
         if args.tile:
             peer.set(kvd.OPT_TILE_BYTES, args.tile)
         if args.threads:
@@ -471,15 +468,12 @@ def run_kvd(args, rank, world, local_rank):
     stats = {"dev_s": dev_s, "wall_s": wall if peer else 0.0, "bytes": bytes_per * K if peer else 0,
              "kern_ms": float(np.mean(kern_ms)) if kern_ms else 0.0,
              "lat": lat_ns, "clock": sampler.summary(), "info": info, "base": base}
-    all_stats = [None] * world if multi else [stats]
-    if multi:
-        dist.all_gather_object(all_stats, stats, group=gloo)
+    all_stats = cluster.gather_stats(stats, gloo) if multi else [stats]
 
     if rank == 0:
         dec = [s for s in all_stats if s["bytes"]]
-        t_dev = max(s["dev_s"] for s in dec)
-        t_wall = max(s["wall_s"] for s in dec)
-        total = sum(s["bytes"] for s in dec)
+        agg = cluster.aggregate(all_stats)          # max time / sum bytes over ranks
+        t_dev, t_wall, total = agg["dev_s"], agg["wall_s"], agg["bytes"]
         lat_all = [x for s in dec for x in s["lat"]]
         kern = max(s["kern_ms"] for s in dec)
         info0 = dec[0]["info"]
@@ -576,7 +570,9 @@ def main():
     ap.add_argument("--impl", choices=["kvd", "reference"], default="kvd")
     ap.add_argument("--config", choices=["c1", "c2", "c4"], default="c2")
     ap.add_argument("--table", choices=["fragmented", "contiguous", "worst"], default="fragmented")
-    ap.add_argument("--variant", choices=["lsu", "lsu32", "ce"], default=None)
+    ap.add_argument("--variant", choices=["lsu", "lsu32", "ce", "tma"], default=None,
+                    help="default: library auto (TMA ring over NVLink, LSU in loopback)")
+    ap.add_argument("--stages", type=int, default=0)
     ap.add_argument("--tile", type=int, default=0)
     ap.add_argument("--threads", type=int, default=0)
     ap.add_argument("--max-ctas", type=int, default=0)

@@ -923,7 +923,12 @@ static kvd_status transfer(kvd_peer p, uint64_t request_id, const int32_t* src_i
     uint32_t max_ctas = p->max_ctas;
     if (!max_ctas) {
       if (tma_defaults) {
-        max_ctas = 32;
+        // enough rings to keep ~4.5 MiB of reads in flight (NVLink round trip
+        // under load ~4.5 us at ~800 GB/s); at least 32 CTAs
+        const uint64_t avg_tile = std::max<uint64_t>(16, info.bytes / std::max(1u, a.total_tiles));
+        const uint64_t per_cta = (uint64_t)(threads / 32) * (stages - 1) * avg_tile;
+        const uint64_t want = ((4608ull << 10) + per_cta - 1) / per_cta;
+        max_ctas = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(want, 32), (uint64_t)p->sm_count);
       } else {
         const int per_sm = kvd::pull_ctas_per_sm(variant, threads, a.nruns);
         max_ctas = (uint32_t)(p->sm_count * per_sm);
