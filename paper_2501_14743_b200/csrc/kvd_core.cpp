@@ -830,11 +830,17 @@ static kvd_status transfer(kvd_peer p, uint64_t request_id, const int32_t* src_i
   // AUTO: over NVLink the TMA ring (1 pipe x 6 stages x 32 KiB per CTA, 32
   // CTAs) saturates the link with ~22% of the SMs; in loopback (both caches
   // on this GPU) the copy is HBM-bound and the full-grid LSU mover is used.
+  // Small requests (<= 2 MiB, e.g. C1) are latency-bound: one warp per CTA
+  // and 2 KiB tiles spread the bytes over as many SMs as possible so the
+  // whole request costs one NVLink round trip.
   const bool over_link = p->remote_device != p->local->device;
   const bool autov = p->variant == KVD_VARIANT_AUTO;
-  int variant = autov ? (over_link ? KVD_VARIANT_TMA : KVD_VARIANT_LSU) : p->variant;
+  const uint64_t req_bytes = (uint64_t)n * NL * 2 * sg.span_bytes;
+  const bool small = autov && req_bytes <= (2ull << 20);
+  int variant = autov ? ((over_link && !small) ? KVD_VARIANT_TMA : KVD_VARIANT_LSU) : p->variant;
   const bool tma_defaults = variant == KVD_VARIANT_TMA && autov;
-  const uint32_t tile = (tma_defaults && !p->tile_set) ? 32768u : p->tile_bytes;
+  const uint32_t tile = p->tile_set ? p->tile_bytes
+                                    : (tma_defaults ? 32768u : (small ? 2048u : p->tile_bytes));
   uint32_t stages = (tma_defaults && !p->stages_set) ? 6u : p->stages;
   if (n) {
     s = tile_runs(p->runs, pp, NL, tile, p->runs4, a);
@@ -851,6 +857,7 @@ static kvd_status transfer(kvd_peer p, uint64_t request_id, const int32_t* src_i
   a.counter = p->counters + slot;
   a.flag = p->flags_dev + slot;
   a.token = token;
+  a.remote_stores = push ? 1u : 0u;
 
   DeviceGuard dgd(p->local->device);
   if (!dgd.ok) return fail(KVD_ECUDA, "cannot select device %d", p->local->device);
@@ -906,7 +913,8 @@ static kvd_status transfer(kvd_peer p, uint64_t request_id, const int32_t* src_i
       info.launches = 1;   // the H2D copy (not a kernel)
     }
     const uint32_t threads =
-        p->threads_set ? p->threads : (variant == KVD_VARIANT_TMA ? (tma_defaults ? 32u : 96u) : 512u);
+        p->threads_set ? p->threads
+                       : (variant == KVD_VARIANT_TMA ? (tma_defaults ? 32u : 96u) : (small ? 32u : 512u));
     if (variant == KVD_VARIANT_TMA) {
       uint64_t smem = (uint64_t)(threads / 32) * stages * a.tile_bytes;
       if (tma_defaults && !p->stages_set && smem > 225u * 1024u) {   // auto: shrink the ring
@@ -917,8 +925,6 @@ static kvd_status transfer(kvd_peer p, uint64_t request_id, const int32_t* src_i
         return fail(KVD_EINVAL, "TMA ring needs %llu B of shared memory (pipes %u x stages %u x "
                     "tile %u); max 225 KiB", (unsigned long long)smem, threads / 32, stages,
                     a.tile_bytes);
-    } else if (threads < 128) {
-      return fail(KVD_EINVAL, "LSU variants need >= 128 threads per CTA");
     }
     uint32_t max_ctas = p->max_ctas;
     if (!max_ctas) {

@@ -40,6 +40,7 @@ struct PullArgs {
   unsigned long long* flag;         // per-slot completion word (pinned, host-mapped)
   unsigned long long token;         // value stored to *flag when every byte has landed
   const int4* runs_dev;             // run table in device memory when nruns > params capacity
+  unsigned int remote_stores;       // 1: stores target a peer GPU (push) -> system-scope fences
 };
 
 enum Variant : int { kLsu16 = 1, kLsu32 = 2, kTma = 4 };

@@ -24,6 +24,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "kvd_internal.h"
 
 namespace kvd {
@@ -31,6 +33,7 @@ namespace {
 
 // Param-resident run tables.  CUDA 12.1+ allows 32764 bytes of kernel
 // parameters; PullArgs is ~160 B, so 2016 int4 runs fit.
+constexpr int kRunsTiny = 8;      // small requests: keep the launch's parameter block short
 constexpr int kRunsSmall = 64;
 constexpr int kRunsMid = 512;
 constexpr int kRunsLarge = 2016;
@@ -137,13 +140,14 @@ __device__ __forceinline__ unsigned int tile_addr(const PullArgs& a, const int4*
   return avail < a.tile_bytes ? (unsigned int)avail : a.tile_bytes;
 }
 
-// Completion (row a6): every thread orders its stores at system scope (in
-// push mode they went to a peer GPU), the CTA arrives once; the last CTA
-// resets the slot counter and publishes the token with a system-scope
-// release, so a host acquire load of the word implies every byte landed.
+// Completion (row a6): every thread orders its stores (gpu scope for the
+// pull's local stores, system scope when push stored into a peer GPU), the
+// CTA arrives once; the last CTA resets the slot counter and publishes the
+// token with a system-scope release, so a host acquire load of the word
+// implies every byte landed.
 __device__ __forceinline__ void complete(const PullArgs& a) {
   if (a.counter == nullptr) return;   // baseline gather/scatter: stream order only
-  __threadfence_system();
+  if (a.remote_stores) __threadfence_system(); else __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
     const unsigned int prev = atomicAdd(a.counter, 1u);
@@ -296,11 +300,20 @@ cudaError_t launch_tma_t(const PullArgs& args, const int4* runs_host, unsigned i
   PullParams<MAXR> P;
   fill(P, args, runs_host);
   const size_t smem = (size_t)(threads / 32) * stages * args.tile_bytes;
-  // per function and device (the static mbarrier array counts against the
-  // 48 KiB default too); cheap, so set on every launch
-  cudaError_t e = cudaFuncSetAttribute(pull_kernel_tma<MAXR>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
+  // The opt-in limit is per function and device (the static mbarrier array
+  // counts against the 48 KiB default too): raise it once per device to the
+  // maximum and remember that.
+  static std::atomic<unsigned long long> raised{0};   // bit d: device d done
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (!(raised.load(std::memory_order_relaxed) & bit)) {
+    cudaError_t e = cudaFuncSetAttribute(pull_kernel_tma<MAXR>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         225 * 1024);
+    if (e != cudaSuccess) return e;
+    raised.fetch_or(bit);
+  }
   pull_kernel_tma<MAXR><<<ctas, threads, smem, stream>>>(P, stages);
   return cudaGetLastError();
 }
@@ -308,6 +321,8 @@ cudaError_t launch_tma_t(const PullArgs& args, const int4* runs_host, unsigned i
 template <typename V, int U>
 cudaError_t launch_v(const PullArgs& args, const int4* runs_host, unsigned int ctas,
                      unsigned int threads, cudaStream_t stream) {
+  if (args.nruns <= (unsigned)kRunsTiny)
+    return launch_t<kRunsTiny, V, U>(args, runs_host, ctas, threads, stream);
   if (args.nruns <= (unsigned)kRunsSmall)
     return launch_t<kRunsSmall, V, U>(args, runs_host, ctas, threads, stream);
   if (args.nruns <= (unsigned)kRunsMid)
@@ -319,6 +334,8 @@ cudaError_t launch_v(const PullArgs& args, const int4* runs_host, unsigned int c
 
 cudaError_t launch_tma(const PullArgs& args, const int4* runs_host, unsigned int ctas,
                        unsigned int threads, unsigned int stages, cudaStream_t stream) {
+  if (args.nruns <= (unsigned)kRunsTiny)
+    return launch_tma_t<kRunsTiny>(args, runs_host, ctas, threads, stages, stream);
   if (args.nruns <= (unsigned)kRunsSmall)
     return launch_tma_t<kRunsSmall>(args, runs_host, ctas, threads, stages, stream);
   if (args.nruns <= (unsigned)kRunsMid)

@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import threading
 from typing import Optional, Sequence
 
 import numpy as np
@@ -88,8 +89,9 @@ _SIGS = {
     "kvd_open_peer": [_p, _p, ctypes.c_size_t, ctypes.POINTER(_p)],
     "kvd_close_peer": [_p],
     "kvd_peer_set": [_p, ctypes.c_int, _i64],
-    "kvd_pull": [_p, _u64, _pi32, _pi32, _u32, _p],
-    "kvd_push": [_p, _u64, _pi32, _pi32, _u32, _p],
+    # hot path: block-id arrays passed as raw addresses (no ctypes pointer objects)
+    "kvd_pull": [_p, _u64, _p, _p, _u32, _p],
+    "kvd_push": [_p, _u64, _p, _p, _u32, _p],
     "kvd_poll_done": [_p, _u64, ctypes.POINTER(ctypes.c_int)],
     "kvd_wait_done": [_p, _u64, _i64],
     "kvd_last_pull_info": [_p, ctypes.POINTER(kvd_pull_info)],
@@ -211,25 +213,46 @@ def kvd_peer_set(peer: int, option: int, value: int) -> None:
     _check(_lib.kvd_peer_set(peer, option, int(value)), "kvd_peer_set")
 
 
+def _addr(a: np.ndarray):
+    return a.__array_interface__["data"][0] if a.size else None
+
+
+def _ids_fast(a) -> np.ndarray:
+    if type(a) is np.ndarray and a.dtype == np.int32 and a.flags.c_contiguous and a.ndim == 1:
+        return a
+    return _ids(a)
+
+
 def kvd_pull(peer: int, request_id: int, src_ids, dst_ids, stream: Optional[int] = None) -> None:
     """`stream`: a cudaStream_t as int (e.g. torch.cuda.current_stream().cuda_stream)."""
-    s, d = _ids(src_ids), _ids(dst_ids)
+    s, d = _ids_fast(src_ids), _ids_fast(dst_ids)
     if s.size != d.size:
         raise ValueError("src_ids and dst_ids differ in length")
-    _check(_lib.kvd_pull(peer, request_id, _ptr_i32(s), _ptr_i32(d), s.size, stream or None),
-           "kvd_pull")
+    st = _lib.kvd_pull(peer, request_id, _addr(s), _addr(d), s.size, stream or None)
+    if st < 0:
+        _check(st, "kvd_pull")
 
 
 def kvd_push(peer: int, request_id: int, src_ids, dst_ids, stream: Optional[int] = None) -> None:
     """Push variant: local blocks src_ids -> remote blocks dst_ids (launch on the local GPU)."""
-    s, d = _ids(src_ids), _ids(dst_ids)
+    s, d = _ids_fast(src_ids), _ids_fast(dst_ids)
     if s.size != d.size:
         raise ValueError("src_ids and dst_ids differ in length")
-    _check(_lib.kvd_push(peer, request_id, _ptr_i32(s), _ptr_i32(d), s.size, stream or None),
-           "kvd_push")
+    st = _lib.kvd_push(peer, request_id, _addr(s), _addr(d), s.size, stream or None)
+    if st < 0:
+        _check(st, "kvd_push")
+
+
+_done = ctypes.c_int(0)
+_done_ref = ctypes.byref(_done)
 
 
 def kvd_poll_done(peer: int, request_id: int) -> bool:
+    if threading.current_thread() is threading.main_thread():
+        st = _lib.kvd_poll_done(peer, request_id, _done_ref)   # reuse one out-cell
+        if st < 0:
+            _check(st, "kvd_poll_done")
+        return bool(_done.value)
     done = ctypes.c_int(0)
     _check(_lib.kvd_poll_done(peer, request_id, ctypes.byref(done)), "kvd_poll_done")
     return bool(done.value)

@@ -37,9 +37,22 @@ def main():
     configs = [("auto", {}), ("lsu", {kvd.OPT_VARIANT: 1}),
                ("lsu_t128_tile4k", {kvd.OPT_VARIANT: 1, kvd.OPT_THREADS: 128,
                                     kvd.OPT_TILE_BYTES: 4096}),
-               ("tma_tile8k", {kvd.OPT_VARIANT: 4, kvd.OPT_THREADS: 32, kvd.OPT_TILE_BYTES: 8192})]
+               ("tma_tile8k", {kvd.OPT_VARIANT: 4, kvd.OPT_THREADS: 32, kvd.OPT_TILE_BYTES: 8192}),
+               ("tma_tile4k_s2", {kvd.OPT_VARIANT: 4, kvd.OPT_THREADS: 32, kvd.OPT_TILE_BYTES: 4096,
+                                  kvd.OPT_STAGES: 2}),
+               ("lsu_t32_tile4k", {kvd.OPT_VARIANT: 1, kvd.OPT_THREADS: 32, kvd.OPT_TILE_BYTES: 4096}),
+               ("lsu_t32_tile2k", {kvd.OPT_VARIANT: 1, kvd.OPT_THREADS: 32, kvd.OPT_TILE_BYTES: 2048}),
+               ("lsu_t64_tile4k", {kvd.OPT_VARIANT: 1, kvd.OPT_THREADS: 64, kvd.OPT_TILE_BYTES: 4096})]
     stream = torch.cuda.Stream(a.dst_dev)
     rid = 0
+    # ctypes + validation floor: the host-only planner on the same table
+    s, d = tables["fragmented"]
+    t = []
+    for _ in range(2000):
+        t0 = time.perf_counter_ns()
+        kvd.kvd_plan(s, d, 64, 64)
+        t.append(time.perf_counter_ns() - t0)
+    print(json.dumps({"kvd_plan_call_us_p50": np.median(t) / 1e3}), flush=True)
     for cname, opts in configs:
         peer = dst.open_peer(src.export())
         h = peer.handle
