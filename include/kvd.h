@@ -231,6 +231,23 @@ KVD_API kvd_status kvd_pull(kvd_peer peer, uint64_t request_id, const int32_t* s
  * Errors: KVD_EINVAL for an unknown request id. */
 KVD_API kvd_status kvd_poll_done(kvd_peer peer, uint64_t request_id, int* done);
 
+/* Batched drain (§4.2 "Tensor communication",
+ * P:L373-378, fig:queue): pull `num_requests` requests with ONE launch.
+ * Request q is entries [offsets[q], offsets[q+1]) of src_ids/dst_ids
+ * (offsets has num_requests+1 entries, offsets[0] = 0, non-decreasing).
+ * The concatenated table is validated as one queue (destination ids
+ * distinct across the whole batch, else KVD_EINVAL) and coalesced as one:
+ * runs may merge across requests ("Read 0->5 from R1 and Read 1->6 from R2
+ * can be merged").  Each request keeps its own completion slot and
+ * completes as soon as ITS bytes have landed (poll each id with
+ * kvd_poll_done); requests with no entries complete at launch.  Ids must be
+ * distinct and not in flight (KVD_EINVAL / KVD_EBUSY).  Issues one small
+ * host-to-device copy of the descriptor table and one kernel on `stream`.
+ * Not available with KVD_VARIANT_CE (KVD_EINVAL). */
+KVD_API kvd_status kvd_pull_batch(kvd_peer peer, uint32_t num_requests,
+                                  const uint64_t* request_ids, const uint32_t* offsets,
+                                  const int32_t* src_ids, const int32_t* dst_ids, void* stream);
+
 /* Push variant (§4.3 push mode, P:L402,
  * fig:push_pull): launched on the PREFILL GPU, copies local blocks
  * src_ids[i] of the peer's local cache into REMOTE blocks dst_ids[i] of the

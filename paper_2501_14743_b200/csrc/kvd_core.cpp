@@ -400,7 +400,20 @@ struct kvd_peer_s {
   std::vector<uint64_t> slot_seq;           // 0 = free, else the token in flight
   uint32_t cursor = 0;
   uint64_t seq = 0;
-  std::unordered_map<uint64_t, std::pair<uint32_t, uint64_t>> inflight;  // req -> (slot, token)
+  struct InFlight {
+    uint32_t slot;
+    uint64_t token;
+    int32_t batch;                          // batch descriptor buffer, -1 for single pulls
+  };
+  std::unordered_map<uint64_t, InFlight> inflight;
+  unsigned long long* bytectr = nullptr;    // device per-slot byte counters (batched drain)
+  struct BatchBuf {
+    char* dev = nullptr;                    // runs | reqs | tokens | run_pos
+    char* host = nullptr;                   // pinned staging
+    size_t cap = 0;
+    uint32_t refs = 0;                      // requests of the batch not yet retired
+  };
+  std::vector<BatchBuf> batch_bufs;
   std::vector<int4*> slot_runs_dev;         // big run tables (per slot)
   std::vector<uint32_t> slot_runs_cap;
   std::vector<int4*> slot_runs_host;        // pinned staging for the above
@@ -665,6 +678,11 @@ static void peer_release(kvd_peer p) {
   if (p->d_src_bases) cudaFree(p->d_src_bases);
   if (p->flags) cudaFreeHost(p->flags);
   if (p->counters) cudaFree(p->counters);
+  if (p->bytectr) cudaFree(p->bytectr);
+  for (auto& b : p->batch_bufs) {
+    if (b.dev) cudaFree(b.dev);
+    if (b.host) cudaFreeHost(b.host);
+  }
   for (auto q : p->slot_runs_dev) if (q) cudaFree(q);
   for (auto q : p->slot_runs_host) if (q) cudaFreeHost(q);
   delete p;
@@ -739,6 +757,8 @@ kvd_status kvd_open_peer(kvd_cache local, const void* blob, size_t blob_len, kvd
   KVD_CUDA(cudaHostGetDevicePointer((void**)&p->flags_dev, p->flags, 0));
   KVD_CUDA(cudaMalloc(&p->counters, kSlots * sizeof(unsigned int)));
   KVD_CUDA(cudaMemset(p->counters, 0, kSlots * sizeof(unsigned int)));
+  KVD_CUDA(cudaMalloc(&p->bytectr, kSlots * sizeof(unsigned long long)));
+  KVD_CUDA(cudaMemset(p->bytectr, 0, kSlots * sizeof(unsigned long long)));
   KVD_CUDA(cudaDeviceSynchronize());
   p->slot_seq.assign(kSlots, 0);
   p->slot_runs_dev.assign(kSlots, nullptr);
@@ -800,6 +820,69 @@ kvd_status kvd_peer_set(kvd_peer p, int option, int64_t value) {
 // ===========================================================================
 // ABI: a3-a6 pull
 // ===========================================================================
+// Launch policy.  AUTO: over NVLink the TMA ring (1 pipe x 6 stages x 32
+// KiB per CTA, >= 32 CTAs) saturates the link with ~22% of the SMs; in
+// loopback (both caches on this GPU) the copy is HBM-bound and the full-grid
+// LSU mover is used.  Small requests (<= 2 MiB, e.g. C1) are latency-bound:
+// one warp per CTA and 2 KiB tiles spread the bytes over as many SMs as
+// possible so the whole request costs one NVLink round trip.
+struct Policy {
+  int variant;
+  bool autov, small, tma_defaults;
+  uint32_t tile, stages;
+};
+
+static Policy choose_policy(const kvd_peer_s* p, uint64_t req_bytes) {
+  Policy P{};
+  const bool over_link = p->remote_device != p->local->device;
+  P.autov = p->variant == KVD_VARIANT_AUTO;
+  P.small = P.autov && req_bytes <= (2ull << 20);
+  P.variant = P.autov ? ((over_link && !P.small) ? KVD_VARIANT_TMA : KVD_VARIANT_LSU) : p->variant;
+  P.tma_defaults = P.variant == KVD_VARIANT_TMA && P.autov;
+  P.tile = p->tile_set ? p->tile_bytes
+                       : (P.tma_defaults ? 32768u : (P.small ? 2048u : p->tile_bytes));
+  P.stages = (P.tma_defaults && !p->stages_set) ? 6u : p->stages;
+  return P;
+}
+
+// Threads per CTA, TMA ring depth and grid size of a tiled launch.
+static kvd_status launch_shape(const kvd_peer_s* p, Policy& P, const kvd::PullArgs& a,
+                               uint64_t bytes, uint32_t* threads_out, uint32_t* ctas_out) {
+  const uint32_t threads =
+      p->threads_set ? p->threads
+                     : (P.variant == KVD_VARIANT_TMA ? (P.tma_defaults ? 32u : 96u)
+                                                     : (P.small ? 32u : 512u));
+  if (P.variant == KVD_VARIANT_TMA) {
+    uint64_t smem = (uint64_t)(threads / 32) * P.stages * a.tile_bytes;
+    if (P.tma_defaults && !p->stages_set && smem > 225u * 1024u) {   // auto: shrink the ring
+      P.stages = (uint32_t)std::max<uint64_t>(
+          2, (225u * 1024u) / ((threads / 32) * (uint64_t)a.tile_bytes));
+      smem = (uint64_t)(threads / 32) * P.stages * a.tile_bytes;
+    }
+    if (smem > 225u * 1024u)   // 227 KiB per CTA minus the 2 KiB mbarrier array
+      return fail(KVD_EINVAL, "TMA ring needs %llu B of shared memory (pipes %u x stages %u x "
+                  "tile %u); max 225 KiB", (unsigned long long)smem, threads / 32, P.stages,
+                  a.tile_bytes);
+  }
+  uint32_t max_ctas = p->max_ctas;
+  if (!max_ctas) {
+    if (P.tma_defaults) {
+      // enough rings to keep ~4.5 MiB of reads in flight (NVLink round trip
+      // under load ~4.5 us at ~800 GB/s); at least 32 CTAs
+      const uint64_t avg_tile = std::max<uint64_t>(16, bytes / std::max(1u, a.total_tiles));
+      const uint64_t per_cta = (uint64_t)(threads / 32) * (P.stages - 1) * avg_tile;
+      const uint64_t want = ((4608ull << 10) + per_cta - 1) / per_cta;
+      max_ctas = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(want, 32), (uint64_t)p->sm_count);
+    } else {
+      const int per_sm = kvd::pull_ctas_per_sm(P.variant, threads, a.nruns);
+      max_ctas = (uint32_t)(p->sm_count * per_sm);
+    }
+  }
+  *threads_out = threads;
+  *ctas_out = grid_for(a.total_tiles, threads, max_ctas);
+  return KVD_OK;
+}
+
 // Pull (push = false): remote (imported) cache -> local cache, kernel on the
 // local GPU reading over NVLink.  Push (push = true, §8 f2): local cache ->
 // remote cache, kernel on the local GPU storing over NVLink.
@@ -827,23 +910,10 @@ static kvd_status transfer(kvd_peer p, uint64_t request_id, const int32_t* src_i
                         sg.block_stride_bytes};
   a.dst = kvd::SideAddr{push ? p->d_src_bases : p->local->d_bases, 0, 0, dg_.plane_stride_bytes,
                         dg_.block_stride_bytes};
-  // AUTO: over NVLink the TMA ring (1 pipe x 6 stages x 32 KiB per CTA, 32
-  // CTAs) saturates the link with ~22% of the SMs; in loopback (both caches
-  // on this GPU) the copy is HBM-bound and the full-grid LSU mover is used.
-  // Small requests (<= 2 MiB, e.g. C1) are latency-bound: one warp per CTA
-  // and 2 KiB tiles spread the bytes over as many SMs as possible so the
-  // whole request costs one NVLink round trip.
-  const bool over_link = p->remote_device != p->local->device;
-  const bool autov = p->variant == KVD_VARIANT_AUTO;
-  const uint64_t req_bytes = (uint64_t)n * NL * 2 * sg.span_bytes;
-  const bool small = autov && req_bytes <= (2ull << 20);
-  int variant = autov ? ((over_link && !small) ? KVD_VARIANT_TMA : KVD_VARIANT_LSU) : p->variant;
-  const bool tma_defaults = variant == KVD_VARIANT_TMA && autov;
-  const uint32_t tile = p->tile_set ? p->tile_bytes
-                                    : (tma_defaults ? 32768u : (small ? 2048u : p->tile_bytes));
-  uint32_t stages = (tma_defaults && !p->stages_set) ? 6u : p->stages;
+  Policy pol = choose_policy(p, (uint64_t)n * NL * 2 * sg.span_bytes);
+  int variant = pol.variant;
   if (n) {
-    s = tile_runs(p->runs, pp, NL, tile, p->runs4, a);
+    s = tile_runs(p->runs, pp, NL, pol.tile, p->runs4, a);
     if (s != KVD_OK) return s;
   }
   // a6: completion slot
@@ -912,36 +982,11 @@ static kvd_status transfer(kvd_peer p, uint64_t request_id, const int32_t* src_i
       a.runs_dev = p->slot_runs_dev[slot];
       info.launches = 1;   // the H2D copy (not a kernel)
     }
-    const uint32_t threads =
-        p->threads_set ? p->threads
-                       : (variant == KVD_VARIANT_TMA ? (tma_defaults ? 32u : 96u) : (small ? 32u : 512u));
-    if (variant == KVD_VARIANT_TMA) {
-      uint64_t smem = (uint64_t)(threads / 32) * stages * a.tile_bytes;
-      if (tma_defaults && !p->stages_set && smem > 225u * 1024u) {   // auto: shrink the ring
-        stages = (uint32_t)std::max<uint64_t>(2, (225u * 1024u) / ((threads / 32) * (uint64_t)a.tile_bytes));
-        smem = (uint64_t)(threads / 32) * stages * a.tile_bytes;
-      }
-      if (smem > 225u * 1024u)   // 227 KiB per CTA minus the 2 KiB mbarrier array
-        return fail(KVD_EINVAL, "TMA ring needs %llu B of shared memory (pipes %u x stages %u x "
-                    "tile %u); max 225 KiB", (unsigned long long)smem, threads / 32, stages,
-                    a.tile_bytes);
-    }
-    uint32_t max_ctas = p->max_ctas;
-    if (!max_ctas) {
-      if (tma_defaults) {
-        // enough rings to keep ~4.5 MiB of reads in flight (NVLink round trip
-        // under load ~4.5 us at ~800 GB/s); at least 32 CTAs
-        const uint64_t avg_tile = std::max<uint64_t>(16, info.bytes / std::max(1u, a.total_tiles));
-        const uint64_t per_cta = (uint64_t)(threads / 32) * (stages - 1) * avg_tile;
-        const uint64_t want = ((4608ull << 10) + per_cta - 1) / per_cta;
-        max_ctas = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(want, 32), (uint64_t)p->sm_count);
-      } else {
-        const int per_sm = kvd::pull_ctas_per_sm(variant, threads, a.nruns);
-        max_ctas = (uint32_t)(p->sm_count * per_sm);
-      }
-    }
-    const uint32_t ctas = grid_for(a.total_tiles, threads, max_ctas);
-    e = kvd::launch_pull(a, p->runs4.data(), variant, ctas, threads, stages, stream);
+    pol.variant = variant;
+    uint32_t threads = 0, ctas = 0;
+    s = launch_shape(p, pol, a, info.bytes, &threads, &ctas);
+    if (s != KVD_OK) return s;
+    e = kvd::launch_pull(a, p->runs4.data(), variant, ctas, threads, pol.stages, stream);
     info.launches += 1;
     info.ctas = ctas;
     info.threads = threads;
@@ -952,7 +997,7 @@ static kvd_status transfer(kvd_peer p, uint64_t request_id, const int32_t* src_i
   info.variant = (uint32_t)variant;
   p->slot_seq[slot] = token;
   p->cursor = (slot + 1) % kSlots;
-  p->inflight[request_id] = std::make_pair(slot, token);
+  p->inflight[request_id] = kvd_peer_s::InFlight{slot, token, -1};
   p->last = info;
   return KVD_OK;
 }
@@ -967,18 +1012,145 @@ kvd_status kvd_push(kvd_peer p, uint64_t request_id, const int32_t* src_ids,
   return transfer(p, request_id, src_ids, dst_ids, n, stream, true);
 }
 
+// §8 f1: the paper's transaction-queue drain as one launch.
+kvd_status kvd_pull_batch(kvd_peer p, uint32_t num_requests, const uint64_t* request_ids,
+                          const uint32_t* offsets, const int32_t* src_ids, const int32_t* dst_ids,
+                          void* stream_) {
+  if (!p) return fail(KVD_EINVAL, "null peer");
+  if (num_requests == 0) return KVD_OK;
+  if (!request_ids || !offsets) return fail(KVD_EINVAL, "null request table");
+  if (num_requests > kSlots) return fail(KVD_EINVAL, "batch of %u exceeds %u slots", num_requests, kSlots);
+  std::lock_guard<std::mutex> lk(p->mu);
+  if (p->closed) return fail(KVD_ESTATE, "peer closed");
+  if (offsets[0] != 0) return fail(KVD_EINVAL, "offsets[0] must be 0");
+  for (uint32_t q = 0; q < num_requests; ++q)
+    if (offsets[q + 1] < offsets[q]) return fail(KVD_EINVAL, "offsets must be non-decreasing");
+  {
+    std::unordered_map<uint64_t, uint32_t> seen;
+    for (uint32_t q = 0; q < num_requests; ++q) {
+      if (p->inflight.count(request_ids[q]))
+        return fail(KVD_EBUSY, "request %llu already in flight", (unsigned long long)request_ids[q]);
+      if (!seen.emplace(request_ids[q], q).second)
+        return fail(KVD_EINVAL, "request %llu twice in one batch", (unsigned long long)request_ids[q]);
+    }
+  }
+  if (p->variant == KVD_VARIANT_CE) return fail(KVD_EINVAL, "the copy-engine comparator has no batch mode");
+  const uint32_t n = offsets[num_requests];
+  const kvd_geometry& sg = p->remote.g;
+  const kvd_geometry& dg_ = p->local->geom.g;
+  // a3 over the whole drained queue: destinations distinct across the batch
+  // (one launch writes them all), runs may span request boundaries
+  kvd_status s = p->planner.plan(src_ids, dst_ids, n, p->remote.layout.num_blocks,
+                                 p->local->geom.layout.num_blocks, p->coalesce != 0, p->runs);
+  if (s != KVD_OK) return s;
+  const PairPlan pp = pair_plan(sg, dg_);
+  const uint32_t NL = p->local->geom.layout.num_layers;
+  kvd::PullArgs a{};
+  a.src = kvd::SideAddr{p->d_src_bases, 0, 0, sg.plane_stride_bytes, sg.block_stride_bytes};
+  a.dst = kvd::SideAddr{p->local->d_bases, 0, 0, dg_.plane_stride_bytes, dg_.block_stride_bytes};
+  const uint64_t per_entry = (uint64_t)NL * 2 * sg.span_bytes;
+  Policy pol = choose_policy(p, (uint64_t)n * per_entry);
+  if (pol.variant == KVD_VARIANT_LSU32 && !aligned32(a, p->src_bases, p->local->bases))
+    pol.variant = KVD_VARIANT_LSU;
+  s = tile_runs(p->runs, pp, NL, pol.tile, p->runs4, a);
+  if (s != KVD_OK) return s;
+
+  // completion slots, one per request
+  std::vector<uint32_t> slots;
+  for (uint32_t k = 0; k < kSlots && slots.size() < num_requests; ++k) {
+    const uint32_t c = (p->cursor + k) % kSlots;
+    if (p->slot_seq[c] == 0) slots.push_back(c);
+  }
+  if (slots.size() < num_requests)
+    return fail(KVD_EBUSY, "need %u free completion slots (poll finished requests)", num_requests);
+
+  // device descriptor block: runs | reqs | tokens | run_pos
+  const size_t m = p->runs4.size();
+  const size_t off_reqs = m * sizeof(int4);
+  const size_t off_tok = off_reqs + num_requests * sizeof(uint4);
+  const size_t off_pos = off_tok + num_requests * sizeof(unsigned long long);
+  const size_t bytes_needed = off_pos + std::max<size_t>(m, 1) * sizeof(uint32_t);
+  int32_t bi = -1;
+  for (size_t b = 0; b < p->batch_bufs.size(); ++b)
+    if (p->batch_bufs[b].refs == 0 && p->batch_bufs[b].cap >= bytes_needed) { bi = (int32_t)b; break; }
+  DeviceGuard dgd(p->local->device);
+  if (!dgd.ok) return fail(KVD_ECUDA, "cannot select device %d", p->local->device);
+  if (bi < 0) {
+    kvd_peer_s::BatchBuf nb;
+    nb.cap = std::max<size_t>(bytes_needed, 64 << 10);
+    KVD_CUDA(cudaMalloc(&nb.dev, nb.cap));
+    KVD_CUDA(cudaMallocHost(&nb.host, nb.cap));
+    p->batch_bufs.push_back(nb);
+    bi = (int32_t)p->batch_bufs.size() - 1;
+  }
+  kvd_peer_s::BatchBuf& B = p->batch_bufs[bi];
+  std::vector<uint64_t> tokens(num_requests);
+  memcpy(B.host, p->runs4.data(), m * sizeof(int4));
+  for (uint32_t q = 0; q < num_requests; ++q) {
+    const uint64_t total = (uint64_t)(offsets[q + 1] - offsets[q]) * per_entry;
+    tokens[q] = p->seq + 1 + q;
+    const uint4 R = make_uint4(offsets[q], slots[q], (uint32_t)total, (uint32_t)(total >> 32));
+    memcpy(B.host + off_reqs + q * sizeof(uint4), &R, sizeof(uint4));
+  }
+  memcpy(B.host + off_tok, tokens.data(), num_requests * sizeof(uint64_t));
+  {
+    uint32_t pos = 0;
+    for (size_t r = 0; r < m; ++r) {
+      memcpy(B.host + off_pos + r * sizeof(uint32_t), &pos, sizeof(uint32_t));
+      pos += p->runs[r].len;
+    }
+  }
+  cudaStream_t stream = (cudaStream_t)stream_;
+  KVD_CUDA(cudaMemcpyAsync(B.dev, B.host, bytes_needed, cudaMemcpyHostToDevice, stream));
+  a.runs_dev = reinterpret_cast<const int4*>(B.dev);
+  a.nreqs = num_requests;
+  a.reqs = reinterpret_cast<const uint4*>(B.dev + off_reqs);
+  a.tokens = reinterpret_cast<const unsigned long long*>(B.dev + off_tok);
+  a.run_pos = reinterpret_cast<const unsigned int*>(B.dev + off_pos);
+  a.bytectr = p->bytectr;
+  a.flags = p->flags_dev;
+  a.counter = nullptr;                  // per-request completion replaces the CTA arrival
+  a.remote_stores = 0;
+  uint32_t threads = 0, ctas = 0;
+  s = launch_shape(p, pol, a, (uint64_t)n * per_entry, &threads, &ctas);
+  if (s != KVD_OK) return s;
+  cudaError_t e = kvd::launch_pull(a, p->runs4.data(), pol.variant, ctas, threads, pol.stages, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "batched pull launch");
+  p->seq += num_requests;
+  for (uint32_t q = 0; q < num_requests; ++q) {
+    p->slot_seq[slots[q]] = tokens[q];
+    p->inflight[request_ids[q]] = kvd_peer_s::InFlight{slots[q], tokens[q], bi};
+  }
+  B.refs = num_requests;
+  p->cursor = (slots.back() + 1) % kSlots;
+  kvd_pull_info info{};
+  info.request_id = request_ids[0];
+  info.blocks = n;
+  info.runs = (uint32_t)m;
+  info.bytes = (uint64_t)n * per_entry;
+  info.segments = (uint64_t)NL * pp.planes * (pp.contiguous ? m : n);
+  info.tiles = a.total_tiles;
+  info.ctas = ctas;
+  info.threads = threads;
+  info.variant = (uint32_t)pol.variant;
+  info.launches = 2;                    // descriptor upload + one kernel
+  p->last = info;
+  return KVD_OK;
+}
+
 kvd_status kvd_poll_done(kvd_peer p, uint64_t request_id, int* done) {
   if (!p || !done) return fail(KVD_EINVAL, "null argument");
   std::lock_guard<std::mutex> lk(p->mu);
   auto it = p->inflight.find(request_id);
   if (it == p->inflight.end())
     return fail(KVD_EINVAL, "request %llu is not in flight", (unsigned long long)request_id);
-  const uint32_t slot = it->second.first;
-  const uint64_t token = it->second.second;
+  const uint32_t slot = it->second.slot;
+  const uint64_t token = it->second.token;
   const uint64_t v = __atomic_load_n(&p->flags[slot], __ATOMIC_ACQUIRE);
   if (v == token) {
     *done = 1;
     p->slot_seq[slot] = 0;
+    if (it->second.batch >= 0) --p->batch_bufs[it->second.batch].refs;
     p->inflight.erase(it);
   } else {
     *done = 0;

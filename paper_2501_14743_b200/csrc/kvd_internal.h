@@ -41,6 +41,18 @@ struct PullArgs {
   unsigned long long token;         // value stored to *flag when every byte has landed
   const int4* runs_dev;             // run table in device memory when nruns > params capacity
   unsigned int remote_stores;       // 1: stores target a peer GPU (push) -> system-scope fences
+
+  // Batched drain: nreqs > 0 means several requests share
+  // this launch and each is completed on its own.  The concatenated block
+  // table is coalesced as one queue (runs may span requests, fig:queue);
+  // every tile credits its bytes to the request(s) that own its blocks and
+  // the credit that completes a request publishes that request's token.
+  unsigned int nreqs;
+  const unsigned int* run_pos;      // [nruns] position of each run's first entry in the batch
+  const uint4* reqs;                // [nreqs] {first entry, slot, total bytes lo, hi}
+  const unsigned long long* tokens; // [nreqs]
+  unsigned long long* bytectr;      // per-slot byte counters (device, zero when idle)
+  unsigned long long* flags;        // per-slot completion words (pinned, host-mapped)
 };
 
 enum Variant : int { kLsu16 = 1, kLsu32 = 2, kTma = 4 };

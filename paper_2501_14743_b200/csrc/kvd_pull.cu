@@ -103,11 +103,20 @@ __device__ __forceinline__ unsigned long long layer_base(const SideAddr& s, unsi
   return s.table ? s.table[l] : s.base + (unsigned long long)l * s.step;
 }
 
-// Tile t -> (source address, destination address, bytes).  Segments are
-// (layer, plane, run); a tile never crosses one.  runs[r].w is the inclusive
-// tile prefix over runs within one (layer, plane).
-__device__ __forceinline__ unsigned int tile_addr(const PullArgs& a, const int4* runs,
-                                                  unsigned int t, const char*& src, char*& dst) {
+// One work item.  `off` is the tile's byte offset inside its run's units
+// laid end to end ([0, len * unit_bytes)), used to credit batched requests.
+struct Tile {
+  const char* src;
+  char* dst;
+  unsigned int bytes;
+  unsigned int run;
+  unsigned long long off;
+};
+
+// Tile t -> addresses.  Segments are (layer, plane, run); a tile never
+// crosses one.  runs[r].w is the inclusive tile prefix over runs within one
+// (layer, plane).
+__device__ __forceinline__ Tile tile_at(const PullArgs& a, const int4* runs, unsigned int t) {
   const unsigned int lp = t / a.tiles_per_lp;
   const unsigned int k = t - lp * a.tiles_per_lp;
   const unsigned int l = (a.planes == 2) ? (lp >> 1) : lp;
@@ -119,12 +128,13 @@ __device__ __forceinline__ unsigned int tile_addr(const PullArgs& a, const int4*
   }
   const int4 run = runs[lo];
   const unsigned int kr = k - (lo ? (unsigned int)runs[lo - 1].w : 0u);
-  unsigned long long src_off, dst_off, off, avail;
+  unsigned long long src_off, dst_off, off, avail, in_run;
   if (a.contiguous) {
     off = (unsigned long long)kr * a.tile_bytes;
     avail = (unsigned long long)(unsigned int)run.z * a.unit_bytes - off;
     src_off = (unsigned long long)run.x * a.src.block_stride + off;
     dst_off = (unsigned long long)run.y * a.dst.block_stride + off;
+    in_run = off;
   } else {
     const unsigned int j = kr / a.tiles_per_unit;
     const unsigned int kk = kr - j * a.tiles_per_unit;
@@ -132,12 +142,68 @@ __device__ __forceinline__ unsigned int tile_addr(const PullArgs& a, const int4*
     avail = a.unit_bytes - off;
     src_off = (unsigned long long)(run.x + (int)j) * a.src.block_stride + off;
     dst_off = (unsigned long long)(run.y + (int)j) * a.dst.block_stride + off;
+    in_run = (unsigned long long)j * a.unit_bytes + off;
   }
-  src = reinterpret_cast<const char*>(layer_base(a.src, l) +
-                                      (unsigned long long)p * a.src.plane_stride + src_off);
-  dst = reinterpret_cast<char*>(layer_base(a.dst, l) +
-                                (unsigned long long)p * a.dst.plane_stride + dst_off);
-  return avail < a.tile_bytes ? (unsigned int)avail : a.tile_bytes;
+  Tile T;
+  T.src = reinterpret_cast<const char*>(layer_base(a.src, l) +
+                                        (unsigned long long)p * a.src.plane_stride + src_off);
+  T.dst = reinterpret_cast<char*>(layer_base(a.dst, l) +
+                                  (unsigned long long)p * a.dst.plane_stride + dst_off);
+  T.bytes = avail < a.tile_bytes ? (unsigned int)avail : a.tile_bytes;
+  T.run = (unsigned int)lo;
+  T.off = in_run;
+  return T;
+}
+
+// --- batched drain (f1): per-request completion inside one launch ----------
+__device__ __forceinline__ void publish(const PullArgs& a, unsigned int q) {
+  const uint4 R = a.reqs[q];
+  a.bytectr[R.y] = 0ull;                 // slot idle again
+  __threadfence_system();
+  st_release_sys(&a.flags[R.y], a.tokens[q]);
+}
+
+// Credit `bytes` landed bytes to request q; the credit that reaches the
+// request's total publishes it.  Callers fence their stores first.
+__device__ __forceinline__ void credit(const PullArgs& a, unsigned int q, unsigned long long bytes) {
+  const uint4 R = a.reqs[q];
+  const unsigned long long total = (unsigned long long)R.z | ((unsigned long long)R.w << 32);
+  const unsigned long long old = atomicAdd(&a.bytectr[R.y], bytes);
+  if (old + bytes == total) publish(a, q);
+}
+
+// A tile may hold blocks of several requests when runs were merged across
+// requests (fig:queue): split its bytes at the request boundaries.
+__device__ void credit_tile(const PullArgs& a, const Tile& T) {
+  const unsigned int g0 = a.run_pos[T.run];
+  unsigned long long pos = T.off;
+  const unsigned long long end = T.off + T.bytes;
+  while (pos < end) {
+    const unsigned int e = g0 + (unsigned int)(pos / a.unit_bytes);
+    int lo = 0, hi = (int)a.nreqs - 1;          // last request whose first entry <= e
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (a.reqs[mid].x <= e) lo = mid; else hi = mid - 1;
+    }
+    unsigned long long q_end = end;
+    if (lo + 1 < (int)a.nreqs) {
+      const unsigned long long nb = (unsigned long long)(a.reqs[lo + 1].x - g0) * a.unit_bytes;
+      if (nb < q_end) q_end = nb;
+    }
+    credit(a, (unsigned int)lo, q_end - pos);
+    pos = q_end;
+  }
+}
+
+// Requests with no blocks complete at launch.
+__device__ __forceinline__ void publish_empty(const PullArgs& a) {
+  if (a.nreqs == 0 || blockIdx.x != 0 || threadIdx.x != 0) return;
+  for (unsigned int q = 0; q < a.nreqs; ++q)
+    if (a.reqs[q].z == 0 && a.reqs[q].w == 0) publish(a, q);
+}
+
+__device__ __forceinline__ void fence_stores(const PullArgs& a) {
+  if (a.remote_stores) __threadfence_system(); else __threadfence();
 }
 
 // Completion (row a6): every thread orders its stores (gpu scope for the
@@ -170,12 +236,16 @@ pull_kernel(const __grid_constant__ PullParams<MAXR> P) {
   const unsigned int lane = threadIdx.x & 31u;
   const unsigned int warps_per_cta = blockDim.x >> 5;
   const unsigned int nwarps = gridDim.x * warps_per_cta;
+  publish_empty(a);
   for (unsigned int t = blockIdx.x * warps_per_cta + (threadIdx.x >> 5); t < a.total_tiles;
        t += nwarps) {
-    const char* src;
-    char* dst;
-    const unsigned int bytes = tile_addr(a, runs, t, src, dst);
-    warp_copy<V, U>(dst, src, bytes, lane);
+    const Tile T = tile_at(a, runs, t);
+    warp_copy<V, U>(T.dst, T.src, T.bytes, lane);
+    if (a.nreqs) {                        // batched drain: credit this tile's requests
+      fence_stores(a);
+      __syncwarp();
+      if (lane == 0) credit_tile(a, T);
+    }
   }
   complete(a);
 }
@@ -214,6 +284,10 @@ __device__ __forceinline__ void tma_store(void* gdst, const void* smem, unsigned
 __device__ __forceinline__ void tma_wait_read_1() {
   asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
 }
+__device__ __forceinline__ void tma_wait_done_1() {
+  asm volatile("cp.async.bulk.wait_group 1;" ::: "memory");
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
 __device__ __forceinline__ void tma_wait_all() {
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -234,6 +308,7 @@ pull_kernel_tma(const __grid_constant__ PullParams<MAXR> P, unsigned int stages)
   unsigned char* ring = smem + (size_t)warp * S * a.tile_bytes;
   uint64_t* bar = bars + warp * kMaxStages;
 
+  publish_empty(a);
   if ((threadIdx.x & 31u) == 0) {
     for (unsigned int s = 0; s < S; ++s) mbar_init(&bar[s]);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -241,30 +316,39 @@ pull_kernel_tma(const __grid_constant__ PullParams<MAXR> P, unsigned int stages)
     // tile i of this pipe = pipe + i * npipes
     const unsigned int count =
         pipe < a.total_tiles ? (a.total_tiles - pipe + npipes - 1) / npipes : 0u;
-    char* dsts[kMaxStages];
-    unsigned int sizes[kMaxStages];
+    Tile tiles[kMaxStages];
     for (unsigned int k = 0; k < S && k < count; ++k) {
-      const char* src;
-      sizes[k] = tile_addr(a, runs, pipe + k * npipes, src, dsts[k]);
-      tma_load(ring + (size_t)k * a.tile_bytes, src, sizes[k], &bar[k]);
+      tiles[k] = tile_at(a, runs, pipe + k * npipes);
+      tma_load(ring + (size_t)k * a.tile_bytes, tiles[k].src, tiles[k].bytes, &bar[k]);
     }
     for (unsigned int i = 0; i < count; ++i) {
       const unsigned int s = i % S;
       mbar_wait(&bar[s], (i / S) & 1u);
-      tma_store(dsts[s], ring + (size_t)s * a.tile_bytes, sizes[s]);
+      tma_store(tiles[s].dst, ring + (size_t)s * a.tile_bytes, tiles[s].bytes);
       if (i >= 1) {
-        // store i-1 has finished reading its stage: refill it with tile i-1+S
-        tma_wait_read_1();
+        const unsigned int sp = (i - 1) % S;
+        if (a.nreqs) {
+          // batched drain: store i-1 must be COMPLETE (not just read) before
+          // its bytes are credited to their request(s)
+          tma_wait_done_1();
+          fence_stores(a);
+          credit_tile(a, tiles[sp]);
+        } else {
+          tma_wait_read_1();   // store i-1 has finished reading its stage
+        }
+        // refill the stage of tile i-1 with tile i-1+S
         const unsigned int k = i - 1 + S;
         if (k < count) {
-          const unsigned int sk = k % S;
-          const char* src;
-          sizes[sk] = tile_addr(a, runs, pipe + k * npipes, src, dsts[sk]);
-          tma_load(ring + (size_t)sk * a.tile_bytes, src, sizes[sk], &bar[sk]);
+          tiles[sp] = tile_at(a, runs, pipe + k * npipes);
+          tma_load(ring + (size_t)sp * a.tile_bytes, tiles[sp].src, tiles[sp].bytes, &bar[sp]);
         }
       }
     }
     tma_wait_all();
+    if (a.nreqs && count) {
+      fence_stores(a);
+      credit_tile(a, tiles[(count - 1) % S]);
+    }
   }
   __syncwarp();
   complete(a);

@@ -25,7 +25,8 @@ OPT_MAX_CTAS, OPT_TILE_BYTES, OPT_COALESCE, OPT_VARIANT, OPT_THREADS, OPT_STAGES
 EXPORTED = (
     "kvd_layout_geometry", "kvd_plan", "kvd_blob_info", "kvd_register_cache",
     "kvd_unregister_cache", "kvd_export_handle", "kvd_open_peer", "kvd_close_peer",
-    "kvd_peer_set", "kvd_pull", "kvd_push", "kvd_poll_done", "kvd_wait_done", "kvd_last_pull_info",
+    "kvd_peer_set", "kvd_pull", "kvd_push", "kvd_pull_batch", "kvd_poll_done", "kvd_wait_done",
+    "kvd_last_pull_info",
     "kvd_gather", "kvd_scatter", "kvd_strerror", "kvd_last_error", "kvd_abi_version",
 )
 
@@ -92,6 +93,7 @@ _SIGS = {
     # hot path: block-id arrays passed as raw addresses (no ctypes pointer objects)
     "kvd_pull": [_p, _u64, _p, _p, _u32, _p],
     "kvd_push": [_p, _u64, _p, _p, _u32, _p],
+    "kvd_pull_batch": [_p, _u32, _p, _p, _p, _p, _p],
     "kvd_poll_done": [_p, _u64, ctypes.POINTER(ctypes.c_int)],
     "kvd_wait_done": [_p, _u64, _i64],
     "kvd_last_pull_info": [_p, ctypes.POINTER(kvd_pull_info)],
@@ -241,6 +243,26 @@ def kvd_push(peer: int, request_id: int, src_ids, dst_ids, stream: Optional[int]
     st = _lib.kvd_push(peer, request_id, _addr(s), _addr(d), s.size, stream or None)
     if st < 0:
         _check(st, "kvd_push")
+
+
+def kvd_pull_batch(peer: int, request_ids, tables, stream: Optional[int] = None) -> None:
+    """Batched drain: `tables` is a list of (src_ids, dst_ids), one per request id."""
+    ids = np.ascontiguousarray(np.asarray(request_ids, dtype=np.uint64).reshape(-1))
+    if ids.size != len(tables):
+        raise ValueError("one (src_ids, dst_ids) pair per request id")
+    srcs = [_ids(s) for s, _ in tables]
+    dsts = [_ids(d) for _, d in tables]
+    for s, d in zip(srcs, dsts):
+        if s.size != d.size:
+            raise ValueError("src_ids and dst_ids differ in length")
+    offsets = np.zeros(ids.size + 1, dtype=np.uint32)
+    offsets[1:] = np.cumsum([s.size for s in srcs])
+    s_all = np.ascontiguousarray(np.concatenate(srcs) if srcs else np.zeros(0, np.int32))
+    d_all = np.ascontiguousarray(np.concatenate(dsts) if dsts else np.zeros(0, np.int32))
+    st = _lib.kvd_pull_batch(peer, ids.size, _addr(ids), _addr(offsets), _addr(s_all),
+                             _addr(d_all), stream or None)
+    if st < 0:
+        _check(st, "kvd_pull_batch")
 
 
 _done = ctypes.c_int(0)

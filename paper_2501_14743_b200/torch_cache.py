@@ -86,6 +86,11 @@ class Peer:
         s = stream if stream is not None else torch.cuda.current_stream(self.local.device)
         kvd.kvd_push(self.handle, request_id, src_ids, dst_ids, s.cuda_stream)
 
+    def pull_batch(self, request_ids, tables, stream: Optional[torch.cuda.Stream] = None):
+        """§8 f1: several requests, one launch, per-request completion."""
+        s = stream if stream is not None else torch.cuda.current_stream(self.local.device)
+        kvd.kvd_pull_batch(self.handle, request_ids, tables, s.cuda_stream)
+
     def poll(self, request_id: int) -> bool:
         return kvd.kvd_poll_done(self.handle, request_id)
 
