@@ -2,23 +2,26 @@
 """bench.py -- KV pull GB/s per GPU pair and p50 per-request transfer latency
 (BASELINE.json metric) for KVDirect's pull path on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c1|c4]
-                    [--table fragmented|contiguous|worst] [--impl kvd|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c1|c3|c4]
+                    [--table fragmented|contiguous|worst] [--batch] [--impl kvd|reference]
 
 N = 1: no NVLink pair exists on one GPU, so the prefill and decode caches
 share cuda:0 (loopback pull, HBM-bound); this is stated in config.pairing.
 N >= 2 (torchrun, one process per GPU): ranks [0, N/2) hold prefill caches,
-ranks [N/2, N) hold decode caches; decode rank N/2 + k pulls from prefill
-rank k (the paper's rail rule "GPU i ... only with GPU i") over
-NVLink 5 / NVSwitch through CUDA IPC.  No collective on the data path.
+ranks [N/2, N) decode caches; decode rank N/2 + k pulls from prefill rank k
+(the paper's rail rule "GPU i ... only with GPU i") over NVLink 5
+/ NVSwitch through CUDA IPC.  No collective on the data path.
 
 A step = one pass of the per-request hot path over
-one C2 request on every pair: kvd_pull (validate + coalesce + one launch)
-and kvd_poll_done until the device-side completion word flips.  Rows a1-a2
-(register, export/open) are the paper's one-time Connect() and run before
-the timed region.  `value` = bytes pulled by all pairs / device time of the
-K steps (CUDA events on the pull stream, max over ranks); `e2e` = the same
-bytes / host wall time from kvd_pull entry to completion observed.
+one batch of synthetic input on every pair: kvd_pull per request (validate +
+coalesce + one launch) -- or one kvd_pull_batch for the whole batch with
+--batch (§8 f1) -- then kvd_poll_done until every request's device-side
+completion word flips.  C1/C2/C4: one request per pair per step; C3: the
+pair's 16 mixed-length requests.  Rows a1-a2 (register, export/open) are the
+paper's one-time Connect() and run before the timed region.
+`value` = bytes pulled by all pairs / device time of the K steps (CUDA events
+on the pull stream, max over ranks); `e2e` = the same bytes / host wall time
+from the first kvd_pull entry to the last completion observed.
 """
 from __future__ import annotations
 
@@ -40,6 +43,7 @@ import kvdgen  # noqa: E402
 METRIC = "KV pull GB/s per GPU pair vs 900 GB/s NVLink; p50 per-request transfer latency"
 NVLINK_NOMINAL_GBS = 900.0
 NVLINK_MEASURED_GBS = 770.0   # B200_PROFILING.md: measured peer copy per direction
+C3_PAIRS = 4                  # C3 is defined on 4P:4D pairs; pair k gets requests i % 4 == k
 
 
 # ---------------------------------------------------------------------------
@@ -115,8 +119,27 @@ class ClockSampler:
                 "reasons": sorted(self.reasons)}
 
 
-def workload(config: str, table: str):
-    """(geometry, tokens, src_ids, dst_ids, description) for a config."""
+DESC = {
+    "c1": "C1 tiny (2 layers, 2 KV heads, head_dim 64, block 16, fp16), one 256-token request",
+    "c2": "C2 Llama-2-7B KV cache (32 layers, 32 KV heads, head_dim 128, block 16, fp16), "
+          "one 8K-token request",
+    "c3": "C3 Llama-2-7B, 64 mixed-length requests U{512..8192} tokens (random.Random(0)), "
+          "fragmented block tables, 16 requests per pair (request i -> pair i % 4)",
+    "c4": "C4 Llama-3-70B TP=4 shard (80 layers, 2 KV heads/shard, head_dim 128, block 16, "
+          "bf16), one 8K-token request per shard",
+}
+
+
+def workload(config: str, table: str, pair_index: int = 0):
+    """(geometry, [(src_ids, dst_ids)] for this pair, description)."""
+    if config == "c3":
+        toks = kvdgen.mixed_request_tokens(kvdgen.C3_REQUESTS, seed=0)
+        mine = [t for i, t in enumerate(toks) if i % C3_PAIRS == pair_index % C3_PAIRS]
+        counts = [kvdgen.blocks_for(t, 16) for t in mine]
+        pool = 6144
+        g = kvdgen.C2.with_blocks(pool)
+        reqs = kvdgen.disjoint_fragmented_tables(counts, pool, pool, seed=3 + pair_index)
+        return g, reqs, DESC["c3"]
     if config == "c1":
         g, tokens = kvdgen.C1, kvdgen.C1_TOKENS
     elif config == "c4":
@@ -130,12 +153,7 @@ def workload(config: str, table: str):
         s, d = kvdgen.fixed_run_table(n, 1, g.num_blocks, g.num_blocks, seed=1)
     else:
         s, d = kvdgen.fragmented_table(n, g.num_blocks, g.num_blocks, seed=1)
-    names = {"c1": "C1 tiny (2 layers, 2 KV heads, head_dim 64, block 16, fp16), 256-token request",
-             "c2": "C2 Llama-2-7B KV cache (32 layers, 32 KV heads, head_dim 128, block 16, fp16), "
-                   "one 8K-token request",
-             "c4": "C4 Llama-3-70B TP=4 shard (80 layers, 2 KV heads/shard, head_dim 128, block 16, "
-                   "bf16), one 8K-token request per shard"}
-    return g, tokens, s, d, names.get(config, names["c2"])
+    return g, [(s, d)], DESC.get(config, DESC["c2"])
 
 
 def cpu_oracle_sample(target_s: float = 12.0):
@@ -175,9 +193,10 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     from oracle import oracle
-    g, tokens, _, _, desc = workload(args.config, args.table)
-    k = 4 if args.config != "c1" else kvdgen.blocks_for(tokens, g.block_size)
+    g, reqs, desc = workload(args.config, args.table)
+    k = 4 if args.config != "c1" else len(reqs[0][0])
     nb = max(2 * k, 8)
+    g = g.with_blocks(nb)
     lb = oracle.layer_nbytes((0,) * 5, nb, g.block_size, g.num_kv_heads, g.head_dim,
                              g.elem_bytes)
     src = [kvdgen.random_bytes(lb, 10 + l) for l in range(g.num_layers)]
@@ -233,22 +252,25 @@ def traffic_from_profile(config: str, nvlink: bool):
         return None
 
 
-def nccl_baselines(args, g, s_ids, d_ids, src, dst, role, rank, half, dev, gloo, fingerprint):
+def nccl_baselines(args, g, reqs, src, dst, role, rank, half, dev, gloo, fingerprint):
     """The measured baseline (north_star: "NCCL send/recv is kept only as the
     measured baseline"), same caches and block tables as the pull.
 
     N1 = the message-passing flow of fig:diff(a): decode sends the
     wanted block ids (step 1), prefill gathers the blocks into a staging
     buffer with a kernel (2) and ncclSend's it (3), decode ncclRecv's and
-    scatters it into its paged cache (4).  Whole request staged at once.
+    scatters it into its paged cache (4).  The whole step is staged at once
+    (one message per step: favourable to NCCL).
     N2 = grouped per-segment send/recv (ncclGroupStart/End via
     batch_isend_irecv), no staging: one send/recv per contiguous (layer,
-    K/V, run) segment straight between the paged caches.
-    Each is timed as host wall per request (max over ranks) and parity-checked
+    K/V, run) segment straight between the paged caches (C1/C2/C4 only).
+    Each is timed as host wall per step (max over ranks) and parity-checked
     (the decode cache is scribbled before each baseline)."""
     import torch
     import torch.distributed as dist
     from paper_2501_14743_b200 import kvd
+    s_ids = np.ascontiguousarray(np.concatenate([s for s, _ in reqs]), dtype=np.int32)
+    d_ids = np.ascontiguousarray(np.concatenate([d for _, d in reqs]), dtype=np.int32)
     n = len(s_ids)
     span = (src or dst).span_bytes
     nb = g.num_blocks
@@ -256,20 +278,8 @@ def nccl_baselines(args, g, s_ids, d_ids, src, dst, role, rank, half, dev, gloo,
     peer_rank = rank + half if role == "prefill" else rank - half
     stream = torch.cuda.current_stream(dev)
     ids_dev = torch.empty(n, dtype=torch.int32, device=f"cuda:{dev}")
-    ids_host = torch.from_numpy(np.ascontiguousarray(s_ids, dtype=np.int32)).pin_memory()
-    runs = kvd.kvd_plan(s_ids, d_ids, nb, nb)
+    ids_host = torch.from_numpy(s_ids).pin_memory()
     out = {}
-
-    def segments(cache, side):
-        views = []
-        for l in range(g.num_layers):
-            layer = cache.layers[l]
-            for p in range(2):
-                for r in runs:
-                    b0 = int(r[side])
-                    off = p * nb * span + b0 * span
-                    views.append(layer[off:off + int(r[2]) * span])
-        return views
 
     def scribble():
         if role == "decode":
@@ -292,22 +302,33 @@ def nccl_baselines(args, g, s_ids, d_ids, src, dst, role, rank, half, dev, gloo,
             dist.send(staging, peer_rank)
         torch.cuda.synchronize(dev)
 
-    seg_views = segments(src, 0) if role == "prefill" else segments(dst, 1)
+    plans = [("n1_gather_send_recv_scatter", n1, args.steps)]
+    seg_views = []
+    if len(reqs) == 1:
+        runs = kvd.kvd_plan(s_ids, d_ids, nb, nb)
+        cache, side = (src, 0) if role == "prefill" else (dst, 1)
+        for l in range(g.num_layers):
+            layer = cache.layers[l]
+            for p in range(2):
+                for r in runs:
+                    off = p * nb * span + int(r[side]) * span
+                    seg_views.append(layer[off:off + int(r[2]) * span])
 
-    def n2():
-        if role == "decode":
-            ids_dev.copy_(ids_host, non_blocking=True)
-            dist.send(ids_dev, peer_rank)
-            ops = [dist.P2POp(dist.irecv, v, peer_rank) for v in seg_views]
-        else:
-            dist.recv(ids_dev, peer_rank)
-            ops = [dist.P2POp(dist.isend, v, peer_rank) for v in seg_views]
-        for w in dist.batch_isend_irecv(ops):
-            w.wait()
-        torch.cuda.synchronize(dev)
+        def n2():
+            if role == "decode":
+                ids_dev.copy_(ids_host, non_blocking=True)
+                dist.send(ids_dev, peer_rank)
+                ops = [dist.P2POp(dist.irecv, v, peer_rank) for v in seg_views]
+            else:
+                dist.recv(ids_dev, peer_rank)
+                ops = [dist.P2POp(dist.isend, v, peer_rank) for v in seg_views]
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+            torch.cuda.synchronize(dev)
 
-    for name, fn, steps in (("n1_gather_send_recv_scatter", n1, args.steps),
-                            ("n2_grouped_segment_send_recv", n2, max(3, min(args.steps, 10)))):
+        plans.append(("n2_grouped_segment_send_recv", n2, max(3, min(args.steps, 10))))
+
+    for name, fn, steps in plans:
         scribble()
         for _ in range(2):
             fn()
@@ -336,17 +357,18 @@ def nccl_baselines(args, g, s_ids, d_ids, src, dst, role, rank, half, dev, gloo,
 def run_kvd(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
-    from paper_2501_14743_b200 import kvd
+    from paper_2501_14743_b200 import cluster, kvd
     from paper_2501_14743_b200.torch_cache import PagedCache
 
     torch.cuda.set_device(local_rank)
     dev = local_rank
-    g, tokens, s_ids, d_ids, desc = workload(args.config, args.table)
-    n = len(s_ids)
-    from paper_2501_14743_b200 import cluster
     multi = world > 1
     me = cluster.role_of(rank, world)
     role, pairs, half = me.role, me.pairs, world // 2
+    pair_index = (rank % half) if multi else 0
+    g, reqs, desc = workload(args.config, args.table, pair_index)
+    n_req = len(reqs)
+    n_blocks = sum(len(s) for s, _ in reqs)
     gloo = dist.new_group(backend="gloo") if multi else None
 
     def new_cache(seed):
@@ -382,14 +404,41 @@ def run_kvd(args, rank, world, local_rank):
 
     stream = torch.cuda.Stream(dev)
     rid = [rank * 10_000_000]
+    launches = [0]
 
-    def one_pull():
-        rid[0] += 1
-        t0 = time.perf_counter_ns()
-        peer.pull(rid[0], s_ids, d_ids, stream)
-        while not peer.poll(rid[0]):
-            pass
-        return time.perf_counter_ns() - t0
+    def step(lat_out=None, evs=None):
+        """One pass of rows a3-a6 over this pair's requests.  `evs` brackets
+        the launches on the pull stream (the end event is recorded right
+        after the last launch, before the host starts polling)."""
+        ids, t_issue = [], []
+        if evs is not None:
+            evs[0].record(stream)
+        if args.batch:
+            ids = [rid[0] + 1 + q for q in range(n_req)]
+            rid[0] += n_req
+            t0 = time.perf_counter_ns()
+            peer.pull_batch(ids, reqs, stream)
+            t_issue = [t0] * n_req
+            launches[0] += 1
+        else:
+            for s, d in reqs:
+                rid[0] += 1
+                ids.append(rid[0])
+                t_issue.append(time.perf_counter_ns())
+                peer.pull(rid[0], s, d, stream)
+                launches[0] += 1
+        if evs is not None:
+            evs[1].record(stream)
+        pending = list(range(n_req))
+        while pending:
+            still = []
+            for q in pending:
+                if peer.poll(ids[q]):
+                    if lat_out is not None:
+                        lat_out.append(time.perf_counter_ns() - t_issue[q])
+                else:
+                    still.append(q)
+            pending = still
 
     def barrier():
         torch.cuda.synchronize()
@@ -398,7 +447,7 @@ def run_kvd(args, rank, world, local_rank):
 
     for _ in range(args.warmup):
         if peer:
-            one_pull()
+            step()
     barrier()
 
     K = args.steps
@@ -408,66 +457,64 @@ def run_kvd(args, rank, world, local_rank):
     t_end = torch.cuda.Event(enable_timing=True)
     lat_ns = []
     sampler = ClockSampler(dev)
+    launches[0] = 0
     barrier()
     with sampler:
         wall0 = time.perf_counter()
         if peer:
             t_start.record(stream)
             for k in range(K):
-                ev[k][0].record(stream)
-                rid[0] += 1
-                t0 = time.perf_counter_ns()
-                peer.pull(rid[0], s_ids, d_ids, stream)
-                ev[k][1].record(stream)
-                while not peer.poll(rid[0]):
-                    pass
-                lat_ns.append(time.perf_counter_ns() - t0)
+                step(lat_ns, ev[k])
             t_end.record(stream)
         torch.cuda.synchronize()
         wall = time.perf_counter() - wall0
     barrier()
+    timed_launches = launches[0]
 
     info = peer.info() if peer else {}
     dev_s = t_start.elapsed_time(t_end) / 1e3 if peer else 0.0
-    kern_ms = [a.elapsed_time(b) for a, b in ev]
-    bytes_per = int(info.get("bytes", 0))
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    span = (src or dst).span_bytes
+    bytes_per_step = n_blocks * g.num_layers * 2 * span
 
     # parity of the timed configuration (checked once, after timing)
+    s_all = np.concatenate([s for s, _ in reqs])
+    d_all = np.concatenate([d for _, d in reqs])
+
+    def fp(cache, ids):
+        idx = torch.from_numpy(np.ascontiguousarray(ids)).long().cuda(dev)
+        w = torch.arange(1, cache.span_bytes // 8 + 1, device=f"cuda:{dev}", dtype=torch.int64)
+        return torch.stack([(cache.layers[l].view(2, g.num_blocks, -1)[:, idx]
+                             .view(torch.int64) * w).sum(-1)
+                            for l in range(g.num_layers)]).cpu()
+
     ok = True
-    if peer:
-        span = dst.span_bytes
-        di = torch.from_numpy(d_ids).long().cuda(dev)
-        if role == "both":
-            si = torch.from_numpy(s_ids).long().cuda(dev)
-            for l in range(g.num_layers):
-                ok = ok and torch.equal(dst.layers[l].view(2, g.num_blocks, span)[:, di],
-                                        src.layers[l].view(2, g.num_blocks, span)[:, si])
+    if role == "both":
+        si = torch.from_numpy(s_all).long().cuda(dev)
+        di = torch.from_numpy(d_all).long().cuda(dev)
+        for l in range(g.num_layers):
+            ok = ok and torch.equal(dst.layers[l].view(2, g.num_blocks, span)[:, di],
+                                    src.layers[l].view(2, g.num_blocks, span)[:, si])
     if multi:
         # prefill ranks publish per-(layer, plane, block) fingerprints of the
-        # request's source blocks; decode ranks compare their destination blocks
-        def fp(cache, ids):
-            idx = torch.from_numpy(ids).long().cuda(dev)
-            w = torch.arange(1, cache.span_bytes // 8 + 1, device=f"cuda:{dev}", dtype=torch.int64)
-            return torch.stack([(cache.layers[l].view(2, g.num_blocks, -1)[:, idx]
-                                 .view(torch.int64) * w).sum(-1)
-                                for l in range(g.num_layers)]).cpu()
-        mine = fp(src, s_ids) if role == "prefill" else None
+        # requests' source blocks; decode ranks compare their destination blocks
         fps = [None] * world
-        dist.all_gather_object(fps, mine, group=gloo)
+        dist.all_gather_object(fps, fp(src, s_all) if role == "prefill" else None, group=gloo)
         if role == "decode":
-            ok = bool(torch.equal(fp(dst, d_ids), fps[rank - half]))
+            ok = bool(torch.equal(fp(dst, d_all), fps[me.peer]))
     oks = [None] * world if multi else [ok]
     if multi:
         dist.all_gather_object(oks, bool(ok), group=gloo)
 
     base = {}
     if multi and not args.no_nccl:
-        base = nccl_baselines(args, g, s_ids, d_ids, src, dst, role, rank, half, dev, gloo, fp)
+        base = nccl_baselines(args, g, reqs, src, dst, role, rank, half, dev, gloo, fp)
 
-    # max over ranks
-    stats = {"dev_s": dev_s, "wall_s": wall if peer else 0.0, "bytes": bytes_per * K if peer else 0,
-             "kern_ms": float(np.mean(kern_ms)) if kern_ms else 0.0,
-             "lat": lat_ns, "clock": sampler.summary(), "info": info, "base": base}
+    stats = {"dev_s": dev_s, "wall_s": wall if peer else 0.0,
+             "bytes": bytes_per_step * K if peer else 0,
+             "step_ms": float(np.mean(step_ms)) if step_ms else 0.0,
+             "lat": lat_ns, "clock": sampler.summary(), "info": info, "base": base,
+             "launches": timed_launches, "runs": info.get("runs")}
     all_stats = cluster.gather_stats(stats, gloo) if multi else [stats]
 
     if rank == 0:
@@ -475,27 +522,26 @@ def run_kvd(args, rank, world, local_rank):
         agg = cluster.aggregate(all_stats)          # max time / sum bytes over ranks
         t_dev, t_wall, total = agg["dev_s"], agg["wall_s"], agg["bytes"]
         lat_all = [x for s in dec for x in s["lat"]]
-        kern = max(s["kern_ms"] for s in dec)
+        step_dev = max(s["step_ms"] for s in dec)
         info0 = dec[0]["info"]
-        per_launch = info0["bytes"]
         peaks, peak_src = measured_peaks()
+        achieved_link = bytes_per_step / (step_dev / 1e3) / 1e9
         if multi:
-            roof = {"bound": "nvlink", "achieved": round(per_launch / (kern / 1e3) / 1e9, 1),
+            roof = {"bound": "nvlink", "achieved": round(achieved_link, 1),
                     "peak": NVLINK_MEASURED_GBS, "unit": "GB/s",
-                    "frac": round(per_launch / (kern / 1e3) / 1e9 / NVLINK_MEASURED_GBS, 4),
-                    "frac_of_nominal_900": round(per_launch / (kern / 1e3) / 1e9 /
-                                                 NVLINK_NOMINAL_GBS, 4),
+                    "frac": round(achieved_link / NVLINK_MEASURED_GBS, 4),
+                    "frac_of_nominal_900": round(achieved_link / NVLINK_NOMINAL_GBS, 4),
                     "peak_source": "B200_PROFILING.md measured peer copy per direction "
                                    "(nominal 900)",
-                    "algorithmic_bytes_per_launch": per_launch,
+                    "algorithmic_bytes_per_step": bytes_per_step,
                     "traffic": traffic_from_profile(args.config, True)}
         else:
-            alg = 2 * per_launch   # loopback: every byte is read and written in the same HBM
-            roof = {"bound": "hbm", "achieved": round(alg / (kern / 1e3) / 1e9, 1),
+            alg = 2 * bytes_per_step   # loopback: every byte is read and written in the same HBM
+            roof = {"bound": "hbm", "achieved": round(alg / (step_dev / 1e3) / 1e9, 1),
                     "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                    "frac": round(alg / (kern / 1e3) / 1e9 / peaks["hbm_gbs"], 4),
+                    "frac": round(alg / (step_dev / 1e3) / 1e9 / peaks["hbm_gbs"], 4),
                     "peak_source": peak_src + " hbm_gbs (burst copy, read+write bytes)",
-                    "algorithmic_bytes_per_launch": alg,
+                    "algorithmic_bytes_per_step": alg,
                     "traffic": traffic_from_profile(args.config, False)}
         clk = all_stats[world // 2 if multi else 0]["clock"]
         out = {
@@ -504,14 +550,19 @@ def run_kvd(args, rank, world, local_rank):
             "ms_per_step": round(t_dev / K * 1e3, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {
-                "workload": desc, "table": f"{args.table} (kvdgen seed 1)", "blocks": n,
-                "runs": info0.get("runs"), "bytes_per_request": per_launch,
+                "workload": desc,
+                "table": (f"{args.table} (kvdgen seed 1)" if args.config != "c3"
+                          else "disjoint fragmented (kvdgen seed 3 + pair)"),
+                "requests_per_pair_per_step": n_req, "blocks_per_pair_per_step": n_blocks,
+                "bytes_per_pair_per_step": bytes_per_step, "runs": info0.get("runs"),
                 "pairs": pairs,
                 "pairing": ("loopback: prefill and decode caches on the same GPU (one GPU has "
                             "no NVLink pair)") if not multi else
                            f"{pairs}P:{pairs}D rail pairs, rank k -> rank {pairs}+k over NVLink 5",
                 "parallelism": "loopback" if not multi else f"{pairs}x(1P:1D)",
-                "l2": "no flush: each request moves >= 640 MiB, >> 126 MB L2",
+                "issue": "kvd_pull_batch (one launch per step)" if args.batch
+                         else "one kvd_pull per request",
+                "l2": "no flush: every step moves >= 640 MiB per pair, >> 126 MB L2",
                 "cache_dtype": "fp16" if g.dtype == kvdgen.FP16 else "bf16",
                 "variant": info0.get("variant"), "ctas": info0.get("ctas"),
                 "threads": info0.get("threads"), "tiles": info0.get("tiles"),
@@ -521,33 +572,36 @@ def run_kvd(args, rank, world, local_rank):
                                                  4),
             "p50_latency_ms": round(nearest_rank(lat_all, 50) / 1e6, 4),
             "p90_latency_ms": round(nearest_rank(lat_all, 90) / 1e6, 4),
-            "kernel_ms": round(kern, 4),
+            "step_device_ms": round(step_dev, 4),
             "roofline": roof,
             "e2e": {"value": round(total / t_wall / 1e9, 2), "unit": "GB/s",
-                    "h2d_bytes_per_step": 8 * n * pairs, "d2h_bytes_per_step": 8 * pairs,
+                    "h2d_bytes_per_step": 8 * n_blocks * pairs, "d2h_bytes_per_step": 8 * n_req * pairs,
                     "what": "host wall from kvd_pull entry (host block-id tables -> kernel "
-                            "parameters) to the host observing the pinned completion word"},
-            "gpu_launches": sum(s["info"].get("launches", 0) for s in dec) * K,
+                            "parameters) to the host observing the pinned completion words"},
+            "gpu_launches": sum(s["launches"] for s in dec),
             "parity": bool(all(oks)),
             "clocks": clk,
         }
         if multi and not args.no_nccl:
             nb_out = {}
             for name in ("n1_gather_send_recv_scatter", "n2_grouped_segment_send_recv"):
-                rs = [s["base"][name] for s in all_stats if s["base"] and s["base"][name]["bytes"]]
+                rs = [s["base"][name] for s in all_stats
+                      if s["base"] and name in s["base"] and s["base"][name]["bytes"]]
+                if not rs:
+                    continue
                 t = max(r["wall_s"] for r in rs)
                 tot = sum(r["bytes"] for r in rs)
                 lat = [x for r in rs for x in r["lat"]]
-                oks_b = [s["base"][name]["ok"] for s in all_stats if s["base"]]
+                oks_b = [s["base"][name]["ok"] for s in all_stats if s["base"] and name in s["base"]]
                 nb_out[name] = {"value": round(tot / t / 1e9, 2), "unit": "GB/s",
                                 "gbs_per_pair": round(tot / pairs / t / 1e9, 2),
-                                "p50_latency_ms": round(nearest_rank(lat, 50) * 1e3, 4),
-                                "steps": rs[0]["steps"], "segments_per_request": rs[0]["segments"],
+                                "p50_step_latency_ms": round(nearest_rank(lat, 50) * 1e3, 4),
+                                "steps": rs[0]["steps"], "segments_per_step": rs[0]["segments"],
                                 "parity": bool(all(oks_b))}
             nb_out["kvd_pull_e2e_vs_n1"] = round(
                 out["e2e"]["value"] / nb_out["n1_gather_send_recv_scatter"]["value"], 3)
             nb_out["what"] = ("NCCL 2.28 send/recv via torch.distributed on the same caches and "
-                              "block tables; host wall per request incl. the block-id message")
+                              "block tables; host wall per step incl. the block-id message")
             out["nccl_baseline"] = nb_out
         if not multi and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_oracle_sample()
@@ -563,13 +617,16 @@ def run_kvd(args, rank, world, local_rank):
 
 
 def main():
-    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap = argparse.ArgumentParser(description=__doc__,
+                                 formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["kvd", "reference"], default="kvd")
-    ap.add_argument("--config", choices=["c1", "c2", "c4"], default="c2")
+    ap.add_argument("--config", choices=["c1", "c2", "c3", "c4"], default="c2")
     ap.add_argument("--table", choices=["fragmented", "contiguous", "worst"], default="fragmented")
+    ap.add_argument("--batch", action="store_true",
+                    help="issue each step's requests with one kvd_pull_batch (f1)")
     ap.add_argument("--variant", choices=["lsu", "lsu32", "ce", "tma"], default=None,
                     help="default: library auto (TMA ring over NVLink, LSU in loopback)")
     ap.add_argument("--stages", type=int, default=0)
