@@ -158,6 +158,43 @@ int oracle_pull_tokenwise(const uint8_t* const* src_layers, const int64_t src_st
 }
 
 /*
+ * TP-resharding pull (not in the paper, which keeps the
+ * prefill and decode TP degrees equal).  The prefill shard holds src_heads
+ * KV heads, the decode shard dst_heads >= src_heads; the prefill shard's
+ * heads land at decode heads [head_offset, head_offset + src_heads):
+ *   T_l[dst_ids[i]][kv][t][head_offset + h][d] = S_l[src_ids[i]][kv][t][h][d]
+ * for h < src_heads, every other destination byte unchanged.  E.g. prefill
+ * TP=8 -> decode TP=4: decode shard j pulls prefill shard 2j at offset 0 and
+ * shard 2j+1 at offset src_heads.  Same element loop, same validation.
+ */
+int oracle_pull_heads(const uint8_t* const* src_layers, const int64_t src_stride_in[5],
+                      uint32_t src_num_blocks, uint32_t src_heads, uint8_t* const* dst_layers,
+                      const int64_t dst_stride_in[5], uint32_t dst_num_blocks,
+                      uint32_t dst_heads, uint32_t head_offset, uint32_t num_layers,
+                      uint32_t head_dim, uint32_t block_size, uint32_t elem_bytes,
+                      const int32_t* src_ids, const int32_t* dst_ids, uint32_t n) {
+  if (head_offset + src_heads > dst_heads) return ORACLE_EINVAL;
+  int rc = validate(src_ids, dst_ids, n, src_num_blocks, dst_num_blocks);
+  if (rc != ORACLE_OK) return rc;
+  int64_t ss[5], ds[5];
+  resolve_strides(src_stride_in, src_num_blocks, block_size, src_heads, head_dim, ss);
+  resolve_strides(dst_stride_in, dst_num_blocks, block_size, dst_heads, head_dim, ds);
+  for (uint32_t i = 0; i < n; ++i)
+    for (uint32_t l = 0; l < num_layers; ++l)
+      for (int64_t kv = 0; kv < 2; ++kv)
+        for (int64_t t = 0; t < block_size; ++t)
+          for (int64_t h = 0; h < src_heads; ++h)
+            for (int64_t d = 0; d < head_dim; ++d) {
+              int64_t si[5] = {src_ids[i], kv, t, h, d};
+              int64_t di[5] = {dst_ids[i], kv, t, h + head_offset, d};
+              copy_element(dst_layers[l] + oracle_element_offset(ds, di, elem_bytes),
+                           src_layers[l] + oracle_element_offset(ss, si, elem_bytes),
+                           elem_bytes);
+            }
+  return ORACLE_OK;
+}
+
+/*
  * Single-element read used for sampled checks at full size: the byte
  * address of element (b, kv, t, h, d) of one layer, so a test can compute
  * what one output element must be without materialising the whole cache.

@@ -79,6 +79,12 @@ def _load():
             fn.argtypes = [p_ptr, p_i64, ctypes.c_uint32, p_ptr, p_i64, ctypes.c_uint32,
                            ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
                            ctypes.c_uint32, p_i32, p_i32, ctypes.c_uint32]
+        lib.oracle_pull_heads.restype = ctypes.c_int
+        lib.oracle_pull_heads.argtypes = [p_ptr, p_i64, ctypes.c_uint32, ctypes.c_uint32,
+                                          p_ptr, p_i64, ctypes.c_uint32, ctypes.c_uint32,
+                                          ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
+                                          ctypes.c_uint32, ctypes.c_uint32, p_i32, p_i32,
+                                          ctypes.c_uint32]
         lib.oracle_element_offset.restype = ctypes.c_int64
         lib.oracle_element_offset.argtypes = [p_i64, p_i64, ctypes.c_uint32]
         lib.oracle_default_strides.restype = None
@@ -225,6 +231,22 @@ def pull(src_layers: Sequence[np.ndarray], src_stride, src_num_blocks: int,
               len(src_layers), num_heads, head_dim, block_size, elem_bytes,
               src_ids.ctypes.data_as(p_i32), dst_ids.ctypes.data_as(p_i32),
               int(src_ids.shape[0]))
+
+
+def pull_heads(src_layers, src_stride, src_num_blocks: int, src_heads: int,
+               dst_layers, dst_stride, dst_num_blocks: int, dst_heads: int, head_offset: int,
+               head_dim: int, block_size: int, elem_bytes: int, src_ids, dst_ids) -> int:
+    """§8 f4 TP-resharding pull: source heads land at destination heads
+    [head_offset, head_offset + src_heads) (kvd_oracle.c: oracle_pull_heads)."""
+    lib = _load()
+    src_ids = np.ascontiguousarray(src_ids, dtype=np.int32)
+    dst_ids = np.ascontiguousarray(dst_ids, dtype=np.int32)
+    p_i32 = ctypes.POINTER(ctypes.c_int32)
+    return lib.oracle_pull_heads(
+        _ptrs(src_layers), _i64(src_stride), src_num_blocks, src_heads,
+        _ptrs(dst_layers), _i64(dst_stride), dst_num_blocks, dst_heads, head_offset,
+        len(src_layers), head_dim, block_size, elem_bytes,
+        src_ids.ctypes.data_as(p_i32), dst_ids.ctypes.data_as(p_i32), int(src_ids.shape[0]))
 
 
 def c_element_offset(stride, index, elem_bytes: int) -> int:
