@@ -203,6 +203,22 @@ KVD_API kvd_status kvd_export_handle(kvd_cache cache, void* blob, size_t* blob_l
 KVD_API kvd_status kvd_open_peer(kvd_cache local_dst, const void* blob, size_t blob_len,
                          kvd_peer* out);
 
+/* TP-resharding import (not in the paper, which keeps prefill
+ * and decode TP degrees equal): bind a prefill SHARD cache with H_r KV heads
+ * to heads [head_offset, head_offset + H_r) of the local decode cache (H_l
+ * heads, H_r + head_offset <= H_l).  kvd_pull / kvd_pull_batch on the
+ * returned peer then copy, for every requested block, layer, K/V and token,
+ * the shard's H_r heads into that head slice (a strided copy: block_size
+ * rows of H_r*head_dim elements, destination rows H_l*head_dim apart).
+ * Example: prefill TP=8 -> decode TP=4, decode shard j opens prefill shards
+ * 2j (offset 0) and 2j+1 (offset H_r) and pulls the same block table from
+ * both.  Both caches must use the default (L, H, D) inner order (else
+ * KVD_ELAYOUT); layers, head_dim, block_size and element size must match;
+ * H_r * head_dim * elem and head_offset * head_dim * elem must be multiples
+ * of 16 B.  LSU mover only; kvd_push is not available on such a peer. */
+KVD_API kvd_status kvd_open_peer_heads(kvd_cache local_dst, const void* blob, size_t blob_len,
+                                       uint32_t head_offset, kvd_peer* out);
+
 KVD_API kvd_status kvd_close_peer(kvd_peer peer);
 
 /* Tune a peer (see kvd_option).  KVD_EINVAL on an unknown option/value. */

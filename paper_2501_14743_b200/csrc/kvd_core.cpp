@@ -436,6 +436,10 @@ struct kvd_peer_s {
   std::vector<int4> runs4;
   kvd_pull_info last{};
   bool closed = false;
+  // §8 f4 head-sliced peer (row_bytes > 0): remote unit = block_size rows
+  uint32_t row_bytes = 0;
+  uint32_t dst_row_stride = 0;
+  uint64_t head_offset_bytes = 0;
 };
 
 // ===========================================================================
@@ -688,7 +692,10 @@ static void peer_release(kvd_peer p) {
   delete p;
 }
 
-kvd_status kvd_open_peer(kvd_cache local, const void* blob, size_t blob_len, kvd_peer* out) {
+// head_offset < 0: the plain pair (row b compatibility); >= 0: §8 f4
+// TP-resharding, the remote shard's heads map to local heads starting there.
+static kvd_status open_impl(kvd_cache local, const void* blob, size_t blob_len,
+                            int64_t head_offset, kvd_peer* out) {
   if (!local || !out) return fail(KVD_EINVAL, "null argument");
   *out = nullptr;
   Blob B;
@@ -700,20 +707,44 @@ kvd_status kvd_open_peer(kvd_cache local, const void* blob, size_t blob_len, kvd
   // compatibility (row b): what must be equal
   const kvd_layout& A = local->geom.layout;
   const kvd_layout& R = rg.layout;
-  if (A.num_layers != R.num_layers || A.num_kv_heads != R.num_kv_heads ||
-      A.head_dim != R.head_dim || A.block_size != R.block_size ||
-      elem_size(A.dtype) != elem_size(R.dtype))
+  const bool heads_ok = head_offset < 0 ? A.num_kv_heads == R.num_kv_heads
+                                        : (uint64_t)head_offset + R.num_kv_heads <= A.num_kv_heads;
+  if (A.num_layers != R.num_layers || !heads_ok || A.head_dim != R.head_dim ||
+      A.block_size != R.block_size || elem_size(A.dtype) != elem_size(R.dtype))
     return fail(KVD_ELAYOUT,
-                "incompatible caches: layers %u/%u heads %u/%u head_dim %u/%u block %u/%u elem %u/%u",
-                R.num_layers, A.num_layers, R.num_kv_heads, A.num_kv_heads, R.head_dim, A.head_dim,
-                R.block_size, A.block_size, elem_size(R.dtype), elem_size(A.dtype));
-  if (R.stride[kL] != A.stride[kL] || R.stride[kH] != A.stride[kH] || R.stride[kD] != A.stride[kD])
-    return fail(KVD_ELAYOUT, "incompatible (L, H, D) order between prefill and decode caches");
+                "incompatible caches: layers %u/%u heads %u/%u (offset %lld) head_dim %u/%u "
+                "block %u/%u elem %u/%u", R.num_layers, A.num_layers, R.num_kv_heads,
+                A.num_kv_heads, (long long)head_offset, R.head_dim, A.head_dim, R.block_size,
+                A.block_size, elem_size(R.dtype), elem_size(A.dtype));
+  uint32_t row_bytes = 0;
+  if (head_offset < 0) {
+    if (R.stride[kL] != A.stride[kL] || R.stride[kH] != A.stride[kH] ||
+        R.stride[kD] != A.stride[kD])
+      return fail(KVD_ELAYOUT, "incompatible (L, H, D) order between prefill and decode caches");
+  } else {
+    // head slices need the default inner order on both sides: per token the
+    // H*D elements are contiguous (L stride H*D, H stride D, D stride 1)
+    auto lhd = [](const kvd_layout& X) {
+      return X.stride[kD] == 1 && X.stride[kH] == X.head_dim &&
+             X.stride[kL] == (int64_t)X.num_kv_heads * X.head_dim;
+    };
+    if (!lhd(A) || !lhd(R))
+      return fail(KVD_ELAYOUT, "head-sliced pulls need the (L, H, D) inner order on both sides");
+    const uint32_t e = elem_size(A.dtype);
+    row_bytes = R.num_kv_heads * R.head_dim * e;
+    if (row_bytes % 16 || ((uint64_t)head_offset * R.head_dim * e) % 16)
+      return fail(KVD_ELAYOUT, "head slice rows and offset must be multiples of 16 B");
+  }
 
   std::unique_ptr<kvd_peer_s, void (*)(kvd_peer)> p(new (std::nothrow) kvd_peer_s(), peer_release);
   if (!p) return fail(KVD_ENOMEM, "host allocation");
   p->local = local;
   p->remote = rg;
+  if (head_offset >= 0) {
+    p->row_bytes = row_bytes;
+    p->dst_row_stride = A.num_kv_heads * A.head_dim * elem_size(A.dtype);
+    p->head_offset_bytes = (uint64_t)head_offset * A.head_dim * elem_size(A.dtype);
+  }
   p->remote_device = B.device;
   p->same_process = (B.pid == (int64_t)getpid() && B.nonce == process_nonce());
 
@@ -767,6 +798,15 @@ kvd_status kvd_open_peer(kvd_cache local, const void* blob, size_t blob_len, kvd
   KVD_CUDA(cudaDeviceGetAttribute(&p->sm_count, cudaDevAttrMultiProcessorCount, local->device));
   *out = p.release();
   return KVD_OK;
+}
+
+kvd_status kvd_open_peer(kvd_cache local, const void* blob, size_t blob_len, kvd_peer* out) {
+  return open_impl(local, blob, blob_len, -1, out);
+}
+
+kvd_status kvd_open_peer_heads(kvd_cache local, const void* blob, size_t blob_len,
+                               uint32_t head_offset, kvd_peer* out) {
+  return open_impl(local, blob, blob_len, (int64_t)head_offset, out);
 }
 
 kvd_status kvd_close_peer(kvd_peer p) {
@@ -883,6 +923,23 @@ static kvd_status launch_shape(const kvd_peer_s* p, Policy& P, const kvd::PullAr
   return KVD_OK;
 }
 
+// §8 f4: a head-sliced peer copies each remote (block, K|V) unit -- block_size
+// rows of H_r*head_dim elements -- into a strided head slice of the local
+// block: one tile per unit, LSU mover with row strides.
+static void head_slice_plan(const kvd_peer_s* p, const kvd_geometry& sg, PairPlan& pp,
+                            Policy& pol, kvd::PullArgs& a) {
+  pp.planes = 2;
+  pp.unit = sg.span_bytes;
+  pp.contiguous = false;
+  if (pol.variant != KVD_VARIANT_LSU) pol.variant = KVD_VARIANT_LSU;
+  pol.tma_defaults = false;
+  pol.tile = (uint32_t)sg.span_bytes;
+  a.row_bytes = p->row_bytes;
+  a.src_row_stride = p->row_bytes;
+  a.dst_row_stride = p->dst_row_stride;
+  a.dst_unit_offset = p->head_offset_bytes;
+}
+
 // Pull (push = false): remote (imported) cache -> local cache, kernel on the
 // local GPU reading over NVLink.  Push (push = true, §8 f2): local cache ->
 // remote cache, kernel on the local GPU storing over NVLink.
@@ -903,7 +960,7 @@ static kvd_status transfer(kvd_peer p, uint64_t request_id, const int32_t* src_i
   kvd_status s = p->planner.plan(src_ids, dst_ids, n, SG.layout.num_blocks, DG.layout.num_blocks,
                                  p->coalesce != 0, p->runs);
   if (s != KVD_OK) return s;
-  const PairPlan pp = pair_plan(sg, dg_);
+  PairPlan pp = pair_plan(sg, dg_);
   const uint32_t NL = p->local->geom.layout.num_layers;
   kvd::PullArgs a{};
   a.src = kvd::SideAddr{push ? p->local->d_bases : p->d_src_bases, 0, 0, sg.plane_stride_bytes,
@@ -911,6 +968,11 @@ static kvd_status transfer(kvd_peer p, uint64_t request_id, const int32_t* src_i
   a.dst = kvd::SideAddr{push ? p->d_src_bases : p->local->d_bases, 0, 0, dg_.plane_stride_bytes,
                         dg_.block_stride_bytes};
   Policy pol = choose_policy(p, (uint64_t)n * NL * 2 * sg.span_bytes);
+  if (p->row_bytes) {
+    if (push) return fail(KVD_EINVAL, "kvd_push is not available on a head-sliced peer");
+    if (pol.variant == KVD_VARIANT_CE) return fail(KVD_EINVAL, "no copy-engine head slices");
+    head_slice_plan(p, sg, pp, pol, a);
+  }
   int variant = pol.variant;
   if (n) {
     s = tile_runs(p->runs, pp, NL, pol.tile, p->runs4, a);
@@ -1043,13 +1105,14 @@ kvd_status kvd_pull_batch(kvd_peer p, uint32_t num_requests, const uint64_t* req
   kvd_status s = p->planner.plan(src_ids, dst_ids, n, p->remote.layout.num_blocks,
                                  p->local->geom.layout.num_blocks, p->coalesce != 0, p->runs);
   if (s != KVD_OK) return s;
-  const PairPlan pp = pair_plan(sg, dg_);
+  PairPlan pp = pair_plan(sg, dg_);
   const uint32_t NL = p->local->geom.layout.num_layers;
   kvd::PullArgs a{};
   a.src = kvd::SideAddr{p->d_src_bases, 0, 0, sg.plane_stride_bytes, sg.block_stride_bytes};
   a.dst = kvd::SideAddr{p->local->d_bases, 0, 0, dg_.plane_stride_bytes, dg_.block_stride_bytes};
   const uint64_t per_entry = (uint64_t)NL * 2 * sg.span_bytes;
   Policy pol = choose_policy(p, (uint64_t)n * per_entry);
+  if (p->row_bytes) head_slice_plan(p, sg, pp, pol, a);
   if (pol.variant == KVD_VARIANT_LSU32 && !aligned32(a, p->src_bases, p->local->bases))
     pol.variant = KVD_VARIANT_LSU;
   s = tile_runs(p->runs, pp, NL, pol.tile, p->runs4, a);

@@ -42,6 +42,14 @@ struct PullArgs {
   const int4* runs_dev;             // run table in device memory when nruns > params capacity
   unsigned int remote_stores;       // 1: stores target a peer GPU (push) -> system-scope fences
 
+  // TP-resharding (§8 f4): row_bytes > 0 makes every unit block_size rows
+  // of row_bytes, src_row_stride / dst_row_stride apart, and shifts the
+  // destination by dst_unit_offset (the head slice).  One tile = one unit.
+  unsigned int row_bytes;
+  unsigned int src_row_stride;
+  unsigned int dst_row_stride;
+  unsigned long long dst_unit_offset;
+
   // Batched drain: nreqs > 0 means several requests share
   // this launch and each is completed on its own.  The concatenated block
   // table is coalesced as one queue (runs may span requests, fig:queue);

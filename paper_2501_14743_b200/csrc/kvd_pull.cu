@@ -99,6 +99,36 @@ __device__ __forceinline__ void warp_copy(char* __restrict__ dst, const char* __
   }
 }
 
+// Head-slice copy (§8 f4): the unit is `rows` rows of row_bytes; row r sits
+// at src + r*src_rs and dst + r*dst_rs.  Same batching as warp_copy.
+template <typename V, int U>
+__device__ __forceinline__ void warp_copy_rows(char* __restrict__ dst, const char* __restrict__ src,
+                                               unsigned int bytes, unsigned int lane,
+                                               unsigned int row_bytes, unsigned int src_rs,
+                                               unsigned int dst_rs) {
+  const unsigned int vpr = row_bytes / sizeof(V);
+  const unsigned int nv = bytes / sizeof(V);
+  for (unsigned int i = lane; i < nv; i += 32 * U) {
+    V v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const unsigned int idx = i + u * 32;
+      if (idx < nv) {
+        const unsigned int r = idx / vpr, c = idx - r * vpr;
+        v[u] = ld_peer(reinterpret_cast<const V*>(src + (size_t)r * src_rs) + c);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const unsigned int idx = i + u * 32;
+      if (idx < nv) {
+        const unsigned int r = idx / vpr, c = idx - r * vpr;
+        st_local(reinterpret_cast<V*>(dst + (size_t)r * dst_rs) + c, v[u]);
+      }
+    }
+  }
+}
+
 __device__ __forceinline__ unsigned long long layer_base(const SideAddr& s, unsigned int l) {
   return s.table ? s.table[l] : s.base + (unsigned long long)l * s.step;
 }
@@ -148,7 +178,8 @@ __device__ __forceinline__ Tile tile_at(const PullArgs& a, const int4* runs, uns
   T.src = reinterpret_cast<const char*>(layer_base(a.src, l) +
                                         (unsigned long long)p * a.src.plane_stride + src_off);
   T.dst = reinterpret_cast<char*>(layer_base(a.dst, l) +
-                                  (unsigned long long)p * a.dst.plane_stride + dst_off);
+                                  (unsigned long long)p * a.dst.plane_stride + dst_off +
+                                  a.dst_unit_offset);
   T.bytes = avail < a.tile_bytes ? (unsigned int)avail : a.tile_bytes;
   T.run = (unsigned int)lo;
   T.off = in_run;
@@ -240,7 +271,11 @@ pull_kernel(const __grid_constant__ PullParams<MAXR> P) {
   for (unsigned int t = blockIdx.x * warps_per_cta + (threadIdx.x >> 5); t < a.total_tiles;
        t += nwarps) {
     const Tile T = tile_at(a, runs, t);
-    warp_copy<V, U>(T.dst, T.src, T.bytes, lane);
+    if (a.row_bytes)
+      warp_copy_rows<V, U>(T.dst, T.src, T.bytes, lane, a.row_bytes, a.src_row_stride,
+                           a.dst_row_stride);
+    else
+      warp_copy<V, U>(T.dst, T.src, T.bytes, lane);
     if (a.nreqs) {                        // batched drain: credit this tile's requests
       fence_stores(a);
       __syncwarp();
@@ -284,8 +319,9 @@ __device__ __forceinline__ void tma_store(void* gdst, const void* smem, unsigned
 __device__ __forceinline__ void tma_wait_read_1() {
   asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
 }
-__device__ __forceinline__ void tma_wait_done_1() {
-  asm volatile("cp.async.bulk.wait_group 1;" ::: "memory");
+template <int N>
+__device__ __forceinline__ void tma_wait_done() {   // all but the newest N groups complete
+  asm volatile("cp.async.bulk.wait_group %0;" :: "n"(N) : "memory");
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 __device__ __forceinline__ void tma_wait_all() {
@@ -317,6 +353,11 @@ pull_kernel_tma(const __grid_constant__ PullParams<MAXR> P, unsigned int stages)
     const unsigned int count =
         pipe < a.total_tiles ? (a.total_tiles - pipe + npipes - 1) / npipes : 0u;
     Tile tiles[kMaxStages];
+    // batched drain: a tile is credited to its request(s) only once its bulk
+    // store has COMPLETED; credits lag the stores by kCreditLag groups so the
+    // write-completion latency stays hidden behind the ring.
+    constexpr unsigned int kCreditLag = 4;
+    Tile pend[kCreditLag + 1];
     for (unsigned int k = 0; k < S && k < count; ++k) {
       tiles[k] = tile_at(a, runs, pipe + k * npipes);
       tma_load(ring + (size_t)k * a.tile_bytes, tiles[k].src, tiles[k].bytes, &bar[k]);
@@ -325,17 +366,10 @@ pull_kernel_tma(const __grid_constant__ PullParams<MAXR> P, unsigned int stages)
       const unsigned int s = i % S;
       mbar_wait(&bar[s], (i / S) & 1u);
       tma_store(tiles[s].dst, ring + (size_t)s * a.tile_bytes, tiles[s].bytes);
+      if (a.nreqs) pend[i % (kCreditLag + 1)] = tiles[s];
       if (i >= 1) {
         const unsigned int sp = (i - 1) % S;
-        if (a.nreqs) {
-          // batched drain: store i-1 must be COMPLETE (not just read) before
-          // its bytes are credited to their request(s)
-          tma_wait_done_1();
-          fence_stores(a);
-          credit_tile(a, tiles[sp]);
-        } else {
-          tma_wait_read_1();   // store i-1 has finished reading its stage
-        }
+        tma_wait_read_1();   // store i-1 has finished reading its stage
         // refill the stage of tile i-1 with tile i-1+S
         const unsigned int k = i - 1 + S;
         if (k < count) {
@@ -343,11 +377,17 @@ pull_kernel_tma(const __grid_constant__ PullParams<MAXR> P, unsigned int stages)
           tma_load(ring + (size_t)sp * a.tile_bytes, tiles[sp].src, tiles[sp].bytes, &bar[sp]);
         }
       }
+      if (a.nreqs && i >= kCreditLag) {
+        tma_wait_done<kCreditLag>();          // store i - kCreditLag complete
+        fence_stores(a);
+        credit_tile(a, pend[(i - kCreditLag) % (kCreditLag + 1)]);
+      }
     }
     tma_wait_all();
     if (a.nreqs && count) {
       fence_stores(a);
-      credit_tile(a, tiles[(count - 1) % S]);
+      const unsigned int first = count > kCreditLag ? count - kCreditLag : 0u;
+      for (unsigned int j = first; j < count; ++j) credit_tile(a, pend[j % (kCreditLag + 1)]);
     }
   }
   __syncwarp();

@@ -24,7 +24,8 @@ OPT_MAX_CTAS, OPT_TILE_BYTES, OPT_COALESCE, OPT_VARIANT, OPT_THREADS, OPT_STAGES
 
 EXPORTED = (
     "kvd_layout_geometry", "kvd_plan", "kvd_blob_info", "kvd_register_cache",
-    "kvd_unregister_cache", "kvd_export_handle", "kvd_open_peer", "kvd_close_peer",
+    "kvd_unregister_cache", "kvd_export_handle", "kvd_open_peer", "kvd_open_peer_heads",
+    "kvd_close_peer",
     "kvd_peer_set", "kvd_pull", "kvd_push", "kvd_pull_batch", "kvd_poll_done", "kvd_wait_done",
     "kvd_last_pull_info",
     "kvd_gather", "kvd_scatter", "kvd_strerror", "kvd_last_error", "kvd_abi_version",
@@ -88,6 +89,7 @@ _SIGS = {
     "kvd_unregister_cache": [_p],
     "kvd_export_handle": [_p, _p, ctypes.POINTER(ctypes.c_size_t)],
     "kvd_open_peer": [_p, _p, ctypes.c_size_t, ctypes.POINTER(_p)],
+    "kvd_open_peer_heads": [_p, _p, ctypes.c_size_t, _u32, ctypes.POINTER(_p)],
     "kvd_close_peer": [_p],
     "kvd_peer_set": [_p, ctypes.c_int, _i64],
     # hot path: block-id arrays passed as raw addresses (no ctypes pointer objects)
@@ -204,6 +206,14 @@ def kvd_export_handle(cache: int) -> bytes:
 def kvd_open_peer(local_dst: int, blob: bytes) -> int:
     h = _p()
     _check(_lib.kvd_open_peer(local_dst, blob, len(blob), ctypes.byref(h)), "kvd_open_peer")
+    return h.value
+
+
+def kvd_open_peer_heads(local_dst: int, blob: bytes, head_offset: int) -> int:
+    """§8 f4: bind a prefill shard with fewer KV heads to a head slice."""
+    h = _p()
+    _check(_lib.kvd_open_peer_heads(local_dst, blob, len(blob), head_offset, ctypes.byref(h)),
+           "kvd_open_peer_heads")
     return h.value
 
 

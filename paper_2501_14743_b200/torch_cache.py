@@ -54,6 +54,10 @@ class PagedCache:
     def open_peer(self, blob: bytes) -> "Peer":
         return Peer(self, kvd.kvd_open_peer(self.handle, blob))
 
+    def open_peer_heads(self, blob: bytes, head_offset: int) -> "Peer":
+        """§8 f4: the blob's (fewer) heads land at heads [head_offset, ...)."""
+        return Peer(self, kvd.kvd_open_peer_heads(self.handle, blob, head_offset))
+
     def close(self) -> None:
         if self.handle:
             kvd.kvd_unregister_cache(self.handle)

@@ -1,0 +1,93 @@
+"""§8 f4 -- TP-resharding pulls: decode shard j of a TP=4 decode group pulls
+prefill TP=8 shards 2j and 2j+1 into its two head slices.  Expected bytes
+come from the oracle's head-offset element loop (oracle_pull_heads)."""
+import numpy as np
+import pytest
+import torch
+
+import kvdgen
+from gpu_helpers import assert_layers_equal, cache_for, next_request_id
+from oracle import oracle
+from paper_2501_14743_b200 import kvd
+
+pytestmark = pytest.mark.gpu
+
+
+def _fill(cache, seed):
+    host = [kvdgen.random_bytes(cache.layer_bytes, seed + l) for l in range(len(cache.layers))]
+    for t, h in zip(cache.layers, host):
+        t.copy_(torch.from_numpy(h))
+    return host
+
+
+def _run(src_dev, dst_dev, nl=4, nb=64, hs=1, hd=2, d=128, n=40, batch=False, seed=0):
+    shards = [cache_for(kvdgen.CacheGeom(nl, hs, d, 16, nb, kvdgen.BF16), src_dev)
+              for _ in range(hd // hs)]
+    dst = cache_for(kvdgen.CacheGeom(nl, hd, d, 16, nb, kvdgen.BF16), dst_dev)
+    hosts = [_fill(c, 1000 * (i + 1) + seed) for i, c in enumerate(shards)]
+    expected = _fill(dst, 99 + seed)
+    torch.cuda.synchronize(src_dev)
+    torch.cuda.synchronize(dst_dev)
+    peers = [dst.open_peer_heads(c.export(), i * hs) for i, c in enumerate(shards)]
+    s_ids, d_ids = kvdgen.fragmented_table(n, nb, nb, seed=seed + 3)
+    try:
+        for i, p in enumerate(peers):
+            if batch:
+                half = n // 2
+                rids = [next_request_id(), next_request_id()]
+                p.pull_batch(rids, [(s_ids[:half], d_ids[:half]), (s_ids[half:], d_ids[half:])])
+                for r in rids:
+                    p.wait(r)
+            else:
+                rid = next_request_id()
+                p.pull(rid, s_ids, d_ids)
+                p.wait(rid)
+                assert p.info()["bytes"] == n * nl * 2 * 16 * hs * d * 2
+            rc = oracle.pull_heads(hosts[i], (0,) * 5, nb, hs, expected, (0,) * 5, nb, hd, i * hs,
+                                   d, 16, 2, s_ids, d_ids)
+            assert rc == oracle.OK
+        torch.cuda.synchronize(dst_dev)
+        assert_layers_equal([t.cpu().numpy() for t in dst.layers], expected)
+    finally:
+        for p in peers:
+            p.close()
+        dst.close()
+        for c in shards:
+            c.close()
+
+
+@pytest.mark.parametrize("hs,hd", [(1, 2), (2, 8), (4, 8), (1, 4)])
+def test_tp_resharding_loopback(hs, hd):
+    _run(0, 0, hs=hs, hd=hd, seed=hs * 10 + hd)
+
+
+def test_tp_resharding_batched():
+    _run(0, 0, batch=True, seed=5)
+
+
+def test_head_slice_rejects_bad_offsets():
+    src = cache_for(kvdgen.CacheGeom(2, 2, 128, 16, 8, kvdgen.BF16), 0)
+    dst = cache_for(kvdgen.CacheGeom(2, 3, 128, 16, 8, kvdgen.BF16), 0)
+    try:
+        with pytest.raises(kvd.KvdError) as ei:
+            dst.open_peer_heads(src.export(), 2)          # heads 2..3 of 3
+        assert ei.value.status == kvd.ELAYOUT
+        with pytest.raises(kvd.KvdError) as ei:
+            dst.open_peer(src.export())                   # plain pair: heads must match
+        assert ei.value.status == kvd.ELAYOUT
+        p = dst.open_peer_heads(src.export(), 1)
+        rev = src.open_peer(src.export())
+        rev.close()
+        with pytest.raises(kvd.KvdError):
+            p.push(next_request_id(), [0], [1])           # no push on a head-sliced peer
+        p.close()
+    finally:
+        dst.close()
+        src.close()
+
+
+@pytest.mark.gpu2
+def test_tp_resharding_two_gpus_70b_shapes():
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs")
+    _run(0, 1, nl=80, nb=600, hs=1, hd=2, n=512, seed=7)
