@@ -468,19 +468,24 @@ PairPlan pair_plan(const kvd_geometry& s, const kvd_geometry& d) {
 }
 
 // Fill runs4 (= runs + tile prefix) and the tiling fields of args.
+// run_major (batches): runs4[r].w = inclusive prefix of tiles_r * layers *
+// planes, so each run's tiles are consecutive in tile order.
 kvd_status tile_runs(const std::vector<kvd_run>& runs, const PairPlan& pp, uint32_t num_layers,
-                     uint32_t tile_bytes, std::vector<int4>& runs4, kvd::PullArgs& a) {
+                     uint32_t tile_bytes, std::vector<int4>& runs4, kvd::PullArgs& a,
+                     bool run_major = false) {
   runs4.resize(runs.size());
   const uint64_t tpu = (pp.unit + tile_bytes - 1) / tile_bytes;
+  const uint64_t mult = run_major ? (uint64_t)num_layers * pp.planes : 1u;
   uint64_t acc = 0;
   for (size_t r = 0; r < runs.size(); ++r) {
     const uint64_t t = pp.contiguous ? ((uint64_t)runs[r].len * pp.unit + tile_bytes - 1) / tile_bytes
                                      : (uint64_t)runs[r].len * tpu;
-    acc += t;
+    acc += t * mult;
     if (acc >= 0x7fffffffull) return fail(KVD_ERANGE, "request too large for one launch");
     runs4[r] = make_int4(runs[r].src_start, runs[r].dst_start, (int)runs[r].len, (int)acc);
   }
-  const uint64_t total = acc * num_layers * pp.planes;
+  a.run_major = run_major ? 1u : 0u;
+  const uint64_t total = run_major ? acc : acc * num_layers * pp.planes;
   if (total >= 0x7fffffffull) return fail(KVD_ERANGE, "request too large for one launch");
   a.unit_bytes = pp.unit;
   a.num_layers = num_layers;
@@ -1112,10 +1117,18 @@ kvd_status kvd_pull_batch(kvd_peer p, uint32_t num_requests, const uint64_t* req
   a.dst = kvd::SideAddr{p->local->d_bases, 0, 0, dg_.plane_stride_bytes, dg_.block_stride_bytes};
   const uint64_t per_entry = (uint64_t)NL * 2 * sg.span_bytes;
   Policy pol = choose_policy(p, (uint64_t)n * per_entry);
+  if (pol.autov && pol.variant == KVD_VARIANT_TMA) {
+    // batches: the TMA ring must wait for each store's completion before
+    // crediting it, which costs ~30% of its throughput; the full-grid LSU
+    // mover credits after a warp fence and stays at the link ceiling
+    pol.variant = KVD_VARIANT_LSU;
+    pol.tma_defaults = false;
+    pol.tile = p->tile_bytes;
+  }
   if (p->row_bytes) head_slice_plan(p, sg, pp, pol, a);
   if (pol.variant == KVD_VARIANT_LSU32 && !aligned32(a, p->src_bases, p->local->bases))
     pol.variant = KVD_VARIANT_LSU;
-  s = tile_runs(p->runs, pp, NL, pol.tile, p->runs4, a);
+  s = tile_runs(p->runs, pp, NL, pol.tile, p->runs4, a, /*run_major=*/true);
   if (s != KVD_OK) return s;
 
   // completion slots, one per request

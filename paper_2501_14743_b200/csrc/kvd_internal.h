@@ -56,6 +56,10 @@ struct PullArgs {
   // every tile credits its bytes to the request(s) that own its blocks and
   // the credit that completes a request publishes that request's token.
   unsigned int nreqs;
+  // run-major tile order (batches): runs[r].w is the inclusive prefix of
+  // tiles_r * num_layers * planes over runs, so a run's tiles (all layers and
+  // both planes) are consecutive and requests finish in queue order.
+  unsigned int run_major;
   const unsigned int* run_pos;      // [nruns] position of each run's first entry in the batch
   const uint4* reqs;                // [nreqs] {first entry, slot, total bytes lo, hi}
   const unsigned long long* tokens; // [nreqs]

@@ -147,17 +147,28 @@ struct Tile {
 // crosses one.  runs[r].w is the inclusive tile prefix over runs within one
 // (layer, plane).
 __device__ __forceinline__ Tile tile_at(const PullArgs& a, const int4* runs, unsigned int t) {
-  const unsigned int lp = t / a.tiles_per_lp;
-  const unsigned int k = t - lp * a.tiles_per_lp;
-  const unsigned int l = (a.planes == 2) ? (lp >> 1) : lp;
-  const unsigned int p = (a.planes == 2) ? (lp & 1u) : 0u;
+  unsigned int lp, k;
+  if (a.run_major) {
+    k = t;
+  } else {
+    lp = t / a.tiles_per_lp;
+    k = t - lp * a.tiles_per_lp;
+  }
   int lo = 0, hi = (int)a.nruns - 1;                 // first run with tile_end > k
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
     if ((unsigned int)runs[mid].w > k) hi = mid; else lo = mid + 1;
   }
   const int4 run = runs[lo];
-  const unsigned int kr = k - (lo ? (unsigned int)runs[lo - 1].w : 0u);
+  const unsigned int prev = lo ? (unsigned int)runs[lo - 1].w : 0u;
+  unsigned int kr = k - prev;
+  if (a.run_major) {       // within the run: (layer, plane) major, then tile
+    const unsigned int per_lp = ((unsigned int)run.w - prev) / (a.num_layers * a.planes);
+    lp = kr / per_lp;
+    kr -= lp * per_lp;
+  }
+  const unsigned int l = (a.planes == 2) ? (lp >> 1) : lp;
+  const unsigned int p = (a.planes == 2) ? (lp & 1u) : 0u;
   unsigned long long src_off, dst_off, off, avail, in_run;
   if (a.contiguous) {
     off = (unsigned long long)kr * a.tile_bytes;
@@ -203,25 +214,59 @@ __device__ __forceinline__ void credit(const PullArgs& a, unsigned int q, unsign
   if (old + bytes == total) publish(a, q);
 }
 
+__device__ __forceinline__ void fence_stores(const PullArgs& a) {
+  if (a.remote_stores) __threadfence_system(); else __threadfence();
+}
+
+// Per-warp credit accumulator: a warp's tiles of one request are credited
+// with ONE atomic when the warp moves on to another request (or finishes),
+// after a fence that orders all of the accumulated tiles' stores.  Keeps the
+// current request's entry range to skip the request lookup.
+struct Credit {
+  int q = -1;
+  unsigned int first = 0, next = 0;   // entry range [first, next) of request q
+  unsigned long long bytes = 0;
+};
+
+// LSU: called by every lane of the warp (uniform control flow, warp_sync);
+// each lane fences its own stores, the warp syncs, `lane0` does the atomic.
+// TMA: called by the pipe's single lane after its bulk stores completed.
+__device__ __forceinline__ void credit_flush(const PullArgs& a, Credit& c, bool lane0,
+                                             bool warp_sync) {
+  if (c.q >= 0 && c.bytes) {
+    fence_stores(a);
+    if (warp_sync) __syncwarp();
+    if (lane0) credit(a, (unsigned int)c.q, c.bytes);
+  }
+  c.bytes = 0;
+}
+
 // A tile may hold blocks of several requests when runs were merged across
 // requests (fig:queue): split its bytes at the request boundaries.
-__device__ void credit_tile(const PullArgs& a, const Tile& T) {
+__device__ void credit_tile(const PullArgs& a, const Tile& T, Credit& c, bool lane0,
+                            bool warp_sync) {
   const unsigned int g0 = a.run_pos[T.run];
   unsigned long long pos = T.off;
   const unsigned long long end = T.off + T.bytes;
   while (pos < end) {
     const unsigned int e = g0 + (unsigned int)(pos / a.unit_bytes);
-    int lo = 0, hi = (int)a.nreqs - 1;          // last request whose first entry <= e
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (a.reqs[mid].x <= e) lo = mid; else hi = mid - 1;
+    if (!(c.q >= 0 && e >= c.first && e < c.next)) {
+      int lo = 0, hi = (int)a.nreqs - 1;          // last request whose first entry <= e
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (a.reqs[mid].x <= e) lo = mid; else hi = mid - 1;
+      }
+      credit_flush(a, c, lane0, warp_sync);
+      c.q = lo;
+      c.first = a.reqs[lo].x;
+      c.next = (lo + 1 < (int)a.nreqs) ? a.reqs[lo + 1].x : 0xffffffffu;
     }
     unsigned long long q_end = end;
-    if (lo + 1 < (int)a.nreqs) {
-      const unsigned long long nb = (unsigned long long)(a.reqs[lo + 1].x - g0) * a.unit_bytes;
+    if (c.next != 0xffffffffu) {
+      const unsigned long long nb = (unsigned long long)(c.next - g0) * a.unit_bytes;
       if (nb < q_end) q_end = nb;
     }
-    credit(a, (unsigned int)lo, q_end - pos);
+    c.bytes += q_end - pos;
     pos = q_end;
   }
 }
@@ -231,10 +276,6 @@ __device__ __forceinline__ void publish_empty(const PullArgs& a) {
   if (a.nreqs == 0 || blockIdx.x != 0 || threadIdx.x != 0) return;
   for (unsigned int q = 0; q < a.nreqs; ++q)
     if (a.reqs[q].z == 0 && a.reqs[q].w == 0) publish(a, q);
-}
-
-__device__ __forceinline__ void fence_stores(const PullArgs& a) {
-  if (a.remote_stores) __threadfence_system(); else __threadfence();
 }
 
 // Completion (row a6): every thread orders its stores (gpu scope for the
@@ -268,6 +309,7 @@ pull_kernel(const __grid_constant__ PullParams<MAXR> P) {
   const unsigned int warps_per_cta = blockDim.x >> 5;
   const unsigned int nwarps = gridDim.x * warps_per_cta;
   publish_empty(a);
+  Credit cr;
   for (unsigned int t = blockIdx.x * warps_per_cta + (threadIdx.x >> 5); t < a.total_tiles;
        t += nwarps) {
     const Tile T = tile_at(a, runs, t);
@@ -276,12 +318,9 @@ pull_kernel(const __grid_constant__ PullParams<MAXR> P) {
                            a.dst_row_stride);
     else
       warp_copy<V, U>(T.dst, T.src, T.bytes, lane);
-    if (a.nreqs) {                        // batched drain: credit this tile's requests
-      fence_stores(a);
-      __syncwarp();
-      if (lane == 0) credit_tile(a, T);
-    }
+    if (a.nreqs) credit_tile(a, T, cr, lane == 0, true);   // batched drain
   }
+  if (a.nreqs) credit_flush(a, cr, lane == 0, true);
   complete(a);
 }
 
@@ -358,6 +397,7 @@ pull_kernel_tma(const __grid_constant__ PullParams<MAXR> P, unsigned int stages)
     // write-completion latency stays hidden behind the ring.
     constexpr unsigned int kCreditLag = 4;
     Tile pend[kCreditLag + 1];
+    Credit cr;
     for (unsigned int k = 0; k < S && k < count; ++k) {
       tiles[k] = tile_at(a, runs, pipe + k * npipes);
       tma_load(ring + (size_t)k * a.tile_bytes, tiles[k].src, tiles[k].bytes, &bar[k]);
@@ -379,15 +419,15 @@ pull_kernel_tma(const __grid_constant__ PullParams<MAXR> P, unsigned int stages)
       }
       if (a.nreqs && i >= kCreditLag) {
         tma_wait_done<kCreditLag>();          // store i - kCreditLag complete
-        fence_stores(a);
-        credit_tile(a, pend[(i - kCreditLag) % (kCreditLag + 1)]);
+        credit_tile(a, pend[(i - kCreditLag) % (kCreditLag + 1)], cr, true, false);
       }
     }
     tma_wait_all();
-    if (a.nreqs && count) {
-      fence_stores(a);
+    if (a.nreqs) {
       const unsigned int first = count > kCreditLag ? count - kCreditLag : 0u;
-      for (unsigned int j = first; j < count; ++j) credit_tile(a, pend[j % (kCreditLag + 1)]);
+      for (unsigned int j = first; j < count; ++j)
+        credit_tile(a, pend[j % (kCreditLag + 1)], cr, true, false);
+      credit_flush(a, cr, true, false);
     }
   }
   __syncwarp();
