@@ -304,7 +304,7 @@ def nccl_baselines(args, g, reqs, src, dst, role, rank, half, dev, gloo, fingerp
 
     plans = [("n1_gather_send_recv_scatter", n1, args.steps)]
     seg_views = []
-    if len(reqs) == 1:
+    if len(reqs) == 1 and not getattr(args, "no_n2", False):
         runs = kvd.kvd_plan(s_ids, d_ids, nb, nb)
         cache, side = (src, 0) if role == "prefill" else (dst, 1)
         for l in range(g.num_layers):
@@ -514,7 +514,8 @@ def run_kvd(args, rank, world, local_rank):
              "bytes": bytes_per_step * K if peer else 0,
              "step_ms": float(np.mean(step_ms)) if step_ms else 0.0,
              "lat": lat_ns, "clock": sampler.summary(), "info": info, "base": base,
-             "launches": timed_launches, "runs": info.get("runs")}
+             "launches": timed_launches, "runs": info.get("runs"),
+             "bytes_per_step": bytes_per_step if peer else 0}
     all_stats = cluster.gather_stats(stats, gloo) if multi else [stats]
 
     if rank == 0:
@@ -525,7 +526,10 @@ def run_kvd(args, rank, world, local_rank):
         step_dev = max(s["step_ms"] for s in dec)
         info0 = dec[0]["info"]
         peaks, peak_src = measured_peaks()
-        achieved_link = bytes_per_step / (step_dev / 1e3) / 1e9
+        # per pair: its own bytes over its own launch-bracketed step time
+        per_pair = [s["bytes_per_step"] / (s["step_ms"] / 1e3) / 1e9 for s in dec]
+        achieved_link = float(np.mean(per_pair))
+        bytes_per_step = dec[0]["bytes_per_step"]
         if multi:
             roof = {"bound": "nvlink", "achieved": round(achieved_link, 1),
                     "peak": NVLINK_MEASURED_GBS, "unit": "GB/s",
@@ -534,6 +538,7 @@ def run_kvd(args, rank, world, local_rank):
                     "peak_source": "B200_PROFILING.md measured peer copy per direction "
                                    "(nominal 900)",
                     "algorithmic_bytes_per_step": bytes_per_step,
+                    "per_pair_achieved": [round(x, 1) for x in per_pair],
                     "traffic": traffic_from_profile(args.config, True)}
         else:
             alg = 2 * bytes_per_step   # loopback: every byte is read and written in the same HBM
