@@ -128,8 +128,8 @@ typedef enum {
   KVD_OPT_TILE_BYTES = 1,   /* bytes per warp work item, multiple of 512 (default 16384) */
   KVD_OPT_COALESCE = 2,     /* 1 (default) merge bi-contiguous runs; 0 one run per block (E10 ablation) */
   KVD_OPT_VARIANT = 3,      /* kvd_variant */
-  KVD_OPT_THREADS = 4,      /* threads per CTA: multiple of 32; LSU 32..1024 (default 512);
-                               TMA: threads/32 pipes per CTA, 32..1024 (default 96) */
+  KVD_OPT_THREADS = 4,      /* threads per CTA: multiple of 32; LSU 32..512 (default 512);
+                               TMA: threads/32 pipes per CTA, 32..256 (default 96) */
   KVD_OPT_STAGES = 5        /* TMA ring depth per pipe, 2..8 (default 4); pipes * stages *
                                tile_bytes must fit in 225 KiB of shared memory */
 } kvd_option;

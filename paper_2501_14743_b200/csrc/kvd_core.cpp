@@ -847,8 +847,8 @@ kvd_status kvd_peer_set(kvd_peer p, int option, int64_t value) {
       p->variant = (int)value;
       return KVD_OK;
     case KVD_OPT_THREADS:
-      if (value < 32 || value > 1024 || value % 32)
-        return fail(KVD_EINVAL, "threads must be a multiple of 32 in [32, 1024]");
+      if (value < 32 || value > 512 || value % 32)
+        return fail(KVD_EINVAL, "threads must be a multiple of 32 in [32, 512]");
       p->threads = (uint32_t)value;
       p->threads_set = true;
       return KVD_OK;
@@ -898,6 +898,7 @@ static kvd_status launch_shape(const kvd_peer_s* p, Policy& P, const kvd::PullAr
                      : (P.variant == KVD_VARIANT_TMA ? (P.tma_defaults ? 32u : 96u)
                                                      : (P.small ? 32u : 512u));
   if (P.variant == KVD_VARIANT_TMA) {
+    if (threads > 256) return fail(KVD_EINVAL, "the TMA mover takes at most 8 pipes (256 threads)");
     uint64_t smem = (uint64_t)(threads / 32) * P.stages * a.tile_bytes;
     if (P.tma_defaults && !p->stages_set && smem > 225u * 1024u) {   // auto: shrink the ring
       P.stages = (uint32_t)std::max<uint64_t>(

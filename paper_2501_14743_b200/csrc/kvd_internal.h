@@ -41,6 +41,8 @@ struct PullArgs {
   unsigned long long token;         // value stored to *flag when every byte has landed
   const int4* runs_dev;             // run table in device memory when nruns > params capacity
   unsigned int remote_stores;       // 1: stores target a peer GPU (push) -> system-scope fences
+  unsigned int smem_runs;           // 1: the kernel copies the run table into shared memory
+                                    //    (set by launch_pull when it fits)
 
   // TP-resharding (§8 f4): row_bytes > 0 makes every unit block_size rows
   // of row_bytes, src_row_stride / dst_row_stride apart, and shifts the

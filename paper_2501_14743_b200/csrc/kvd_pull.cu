@@ -297,30 +297,46 @@ __device__ __forceinline__ void complete(const PullArgs& a) {
   }
 }
 
+// Stage the run table in shared memory when the launcher reserved room for
+// it: the per-tile binary search then costs shared loads (~30 cycles)
+// instead of constant-bank / L2 misses, which is what bounds 4-8 KiB
+// segments where a pipe must issue a tile every few hundred nanoseconds.
+__device__ __forceinline__ const int4* stage_runs(const PullArgs& a, const int4* runs,
+                                                  int4* smem_runs) {
+  if (!a.smem_runs) return runs;
+  for (unsigned int i = threadIdx.x; i < a.nruns; i += blockDim.x) smem_runs[i] = runs[i];
+  __syncthreads();
+  return smem_runs;
+}
+
 // ---------------------------------------------------------------------------
 // LSU mover: one warp per tile
 // ---------------------------------------------------------------------------
-template <int MAXR, typename V, int U>
-__global__ void __launch_bounds__(1024)
+// GENERAL = false is the plain single-request copy (no head-slice rows, no
+// batch credits) so the hot path keeps its registers; GENERAL = true adds
+// both.  At most 512 threads per CTA, two CTAs per SM (<= 64 registers).
+template <int MAXR, typename V, int U, bool GENERAL>
+__global__ void __launch_bounds__(512, 2)
 pull_kernel(const __grid_constant__ PullParams<MAXR> P) {
+  extern __shared__ int4 s_runs[];
   const PullArgs& a = P.a;
-  const int4* runs = (MAXR > 0) ? P.runs : a.runs_dev;
+  const int4* runs = stage_runs(a, (MAXR > 0) ? P.runs : a.runs_dev, s_runs);
   const unsigned int lane = threadIdx.x & 31u;
   const unsigned int warps_per_cta = blockDim.x >> 5;
   const unsigned int nwarps = gridDim.x * warps_per_cta;
-  publish_empty(a);
+  if (GENERAL) publish_empty(a);
   Credit cr;
   for (unsigned int t = blockIdx.x * warps_per_cta + (threadIdx.x >> 5); t < a.total_tiles;
        t += nwarps) {
     const Tile T = tile_at(a, runs, t);
-    if (a.row_bytes)
+    if (GENERAL && a.row_bytes)
       warp_copy_rows<V, U>(T.dst, T.src, T.bytes, lane, a.row_bytes, a.src_row_stride,
                            a.dst_row_stride);
     else
       warp_copy<V, U>(T.dst, T.src, T.bytes, lane);
-    if (a.nreqs) credit_tile(a, T, cr, lane == 0, true);   // batched drain
+    if (GENERAL && a.nreqs) credit_tile(a, T, cr, lane == 0, true);   // batched drain
   }
-  if (a.nreqs) credit_flush(a, cr, lane == 0, true);
+  if (GENERAL && a.nreqs) credit_flush(a, cr, lane == 0, true);
   complete(a);
 }
 
@@ -369,17 +385,20 @@ __device__ __forceinline__ void tma_wait_all() {
 }
 
 template <int MAXR>
-__global__ void __launch_bounds__(1024)
+__global__ void __launch_bounds__(256)
 pull_kernel_tma(const __grid_constant__ PullParams<MAXR> P, unsigned int stages) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint64_t bars[32 * kMaxStages];
   const PullArgs& a = P.a;
-  const int4* runs = (MAXR > 0) ? P.runs : a.runs_dev;
   const unsigned int warp = threadIdx.x >> 5;
   const unsigned int pipes_per_cta = blockDim.x >> 5;
   const unsigned int npipes = gridDim.x * pipes_per_cta;
   const unsigned int pipe = blockIdx.x * pipes_per_cta + warp;
   const unsigned int S = stages;
+  // the run table (if staged) sits after all pipes' rings
+  const int4* runs = stage_runs(
+      a, (MAXR > 0) ? P.runs : a.runs_dev,
+      reinterpret_cast<int4*>(smem + (size_t)pipes_per_cta * S * a.tile_bytes));
   unsigned char* ring = smem + (size_t)warp * S * a.tile_bytes;
   uint64_t* bar = bars + warp * kMaxStages;
 
@@ -449,12 +468,23 @@ void fill(PullParams<MAXR>& P, const PullArgs& args, const int4* runs_host) {
     for (unsigned int r = 0; r < args.nruns; ++r) P.runs[r] = runs_host[r];
 }
 
+// Stage run tables of more than 64 runs (a binary search of >= 7 steps) when
+// they fit next to whatever else the kernel keeps in shared memory.
+constexpr unsigned int kStageMinRuns = 64;
+constexpr size_t kStageMaxBytes = 32 * 1024;
+
 template <int MAXR, typename V, int U>
 cudaError_t launch_t(const PullArgs& args, const int4* runs_host, unsigned int ctas,
                      unsigned int threads, cudaStream_t stream) {
   PullParams<MAXR> P;
   fill(P, args, runs_host);
-  pull_kernel<MAXR, V, U><<<ctas, threads, 0, stream>>>(P);
+  const size_t table = (size_t)args.nruns * sizeof(int4);
+  const bool stage = args.nruns > kStageMinRuns && table <= kStageMaxBytes;
+  P.a.smem_runs = stage ? 1u : 0u;
+  if (args.nreqs || args.row_bytes)
+    pull_kernel<MAXR, V, U, true><<<ctas, threads, stage ? table : 0, stream>>>(P);
+  else
+    pull_kernel<MAXR, V, U, false><<<ctas, threads, stage ? table : 0, stream>>>(P);
   return cudaGetLastError();
 }
 
@@ -463,7 +493,12 @@ cudaError_t launch_tma_t(const PullArgs& args, const int4* runs_host, unsigned i
                          unsigned int threads, unsigned int stages, cudaStream_t stream) {
   PullParams<MAXR> P;
   fill(P, args, runs_host);
-  const size_t smem = (size_t)(threads / 32) * stages * args.tile_bytes;
+  const size_t ring = (size_t)(threads / 32) * stages * args.tile_bytes;
+  const size_t table = (size_t)args.nruns * sizeof(int4);
+  const bool stage = args.nruns > kStageMinRuns && table <= kStageMaxBytes &&
+                     ring + table <= 225 * 1024;
+  P.a.smem_runs = stage ? 1u : 0u;
+  const size_t smem = ring + (stage ? table : 0);
   // The opt-in limit is per function and device (the static mbarrier array
   // counts against the 48 KiB default too): raise it once per device to the
   // maximum and remember that.
@@ -512,8 +547,8 @@ cudaError_t launch_tma(const PullArgs& args, const int4* runs_host, unsigned int
 template <int MAXR, typename V, int U>
 int occ(unsigned int threads) {
   int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, pull_kernel<MAXR, V, U>, (int)threads,
-                                                    0) != cudaSuccess)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, pull_kernel<MAXR, V, U, true>,
+                                                    (int)threads, 0) != cudaSuccess)
     return 1;
   return n > 0 ? n : 1;
 }

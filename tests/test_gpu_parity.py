@@ -107,7 +107,7 @@ def test_variants_and_tiles(variant, tile):
         pair.close()
 
 
-@pytest.mark.parametrize("threads,max_ctas", [(128, 1), (1024, 3), (512, 0), (256, 7)])
+@pytest.mark.parametrize("threads,max_ctas", [(128, 1), (512, 3), (512, 0), (256, 7), (32, 0)])
 def test_grid_shapes(threads, max_ctas):
     pair = make_pair(C1, C1, seed=5)
     try:
@@ -410,9 +410,13 @@ def test_tma_ring_shapes(threads, stages, ctas, kind):
 def test_tma_rejects_oversized_ring():
     pair = make_pair(C1, C1, seed=19)
     try:
-        pair.peer.set(kvd.OPT_VARIANT, kvd.VARIANT_TMA).set(kvd.OPT_THREADS, 1024)
+        pair.peer.set(kvd.OPT_VARIANT, kvd.VARIANT_TMA).set(kvd.OPT_THREADS, 256)
+        pair.peer.set(kvd.OPT_STAGES, 8).set(kvd.OPT_TILE_BYTES, 8192)   # 8 x 8 x 8 KiB > 225 KiB
         with pytest.raises(kvd.KvdError) as ei:
             pair.peer.pull(next_request_id(), [0], [1])
+        assert ei.value.status == kvd.EINVAL
+        with pytest.raises(kvd.KvdError) as ei:
+            pair.peer.set(kvd.OPT_THREADS, 1024)             # above the 512-thread bound
         assert ei.value.status == kvd.EINVAL
     finally:
         pair.close()

@@ -47,6 +47,7 @@ def main():
     ap.add_argument("--src-dev", type=int, default=0)
     ap.add_argument("--dst-dev", type=int, default=1)
     ap.add_argument("--config", default="c2")
+    ap.add_argument("--block-size", type=int, default=0, help="override the config's block size")
     ap.add_argument("--tables", default="fragmented")
     ap.add_argument("--variants", default="lsu")
     ap.add_argument("--tiles", default="16384")
@@ -61,6 +62,9 @@ def main():
                     help="one warm-up pull then exactly one pull (for ncu -s/-c)")
     a = ap.parse_args()
     g = geom_of(a.config)
+    if a.block_size:
+        from dataclasses import replace
+        g = replace(g, block_size=a.block_size, num_blocks=g.num_blocks * g.block_size // a.block_size)
     n = kvdgen.blocks_for({"c1": 256, "c2": 8192, "c4": 8192}[a.config], g.block_size)
     mk = lambda dev, seed: PagedCache(g.num_layers, g.num_kv_heads, g.head_dim, g.block_size,
                                       g.num_blocks, g.dtype, g.stride, dev)
