@@ -875,9 +875,20 @@ struct Policy {
   int variant;
   bool autov, small, tma_defaults;
   uint32_t tile, stages;
+  uint32_t pipes;                 // TMA auto: pipes (warps) per CTA
 };
 
-static Policy choose_policy(const kvd_peer_s* p, uint64_t req_bytes) {
+static uint64_t avg_segment(const PairPlan& pp, uint32_t n, size_t runs) {
+  if (!n || !runs) return pp.unit;
+  return pp.contiguous ? (uint64_t)n * pp.unit / runs : pp.unit;
+}
+
+// avg_seg: mean bytes of a contiguous (layer, plane, run) segment.  Short
+// segments (4-16 KiB: fragmented 70B shards, small block sizes) make the TMA
+// ring issue-bound -- one bulk copy per tile per pipe -- so the auto policy
+// then runs several pipes per CTA over smaller stages (C5 sweep: 4 KiB
+// segments 510 -> 747 GB/s with 8 pipes x 4 stages).
+static Policy choose_policy(const kvd_peer_s* p, uint64_t req_bytes, uint64_t avg_seg) {
   Policy P{};
   const bool over_link = p->remote_device != p->local->device;
   P.autov = p->variant == KVD_VARIANT_AUTO;
@@ -887,6 +898,15 @@ static Policy choose_policy(const kvd_peer_s* p, uint64_t req_bytes) {
   P.tile = p->tile_set ? p->tile_bytes
                        : (P.tma_defaults ? 32768u : (P.small ? 2048u : p->tile_bytes));
   P.stages = (P.tma_defaults && !p->stages_set) ? 6u : p->stages;
+  P.pipes = 1;
+  if (P.tma_defaults && avg_seg < (24u << 10)) {
+    uint32_t t = 4096;
+    while (t < avg_seg && t < 16384) t <<= 1;
+    if (!p->tile_set) P.tile = t;
+    if (!p->stages_set) P.stages = 4;
+    P.pipes = std::min<uint32_t>(8, (225u << 10) / (P.stages * P.tile));
+    if (P.pipes > 1 && P.pipes * P.stages * P.tile > (192u << 10)) --P.pipes;
+  }
   return P;
 }
 
@@ -895,7 +915,7 @@ static kvd_status launch_shape(const kvd_peer_s* p, Policy& P, const kvd::PullAr
                                uint64_t bytes, uint32_t* threads_out, uint32_t* ctas_out) {
   const uint32_t threads =
       p->threads_set ? p->threads
-                     : (P.variant == KVD_VARIANT_TMA ? (P.tma_defaults ? 32u : 96u)
+                     : (P.variant == KVD_VARIANT_TMA ? (P.tma_defaults ? 32u * P.pipes : 96u)
                                                      : (P.small ? 32u : 512u));
   if (P.variant == KVD_VARIANT_TMA) {
     if (threads > 256) return fail(KVD_EINVAL, "the TMA mover takes at most 8 pipes (256 threads)");
@@ -973,7 +993,8 @@ static kvd_status transfer(kvd_peer p, uint64_t request_id, const int32_t* src_i
                         sg.block_stride_bytes};
   a.dst = kvd::SideAddr{push ? p->d_src_bases : p->local->d_bases, 0, 0, dg_.plane_stride_bytes,
                         dg_.block_stride_bytes};
-  Policy pol = choose_policy(p, (uint64_t)n * NL * 2 * sg.span_bytes);
+  Policy pol = choose_policy(p, (uint64_t)n * NL * 2 * sg.span_bytes,
+                             avg_segment(pp, n, p->runs.size()));
   if (p->row_bytes) {
     if (push) return fail(KVD_EINVAL, "kvd_push is not available on a head-sliced peer");
     if (pol.variant == KVD_VARIANT_CE) return fail(KVD_EINVAL, "no copy-engine head slices");
@@ -1117,7 +1138,7 @@ kvd_status kvd_pull_batch(kvd_peer p, uint32_t num_requests, const uint64_t* req
   a.src = kvd::SideAddr{p->d_src_bases, 0, 0, sg.plane_stride_bytes, sg.block_stride_bytes};
   a.dst = kvd::SideAddr{p->local->d_bases, 0, 0, dg_.plane_stride_bytes, dg_.block_stride_bytes};
   const uint64_t per_entry = (uint64_t)NL * 2 * sg.span_bytes;
-  Policy pol = choose_policy(p, (uint64_t)n * per_entry);
+  Policy pol = choose_policy(p, (uint64_t)n * per_entry, avg_segment(pp, n, p->runs.size()));
   if (pol.autov && pol.variant == KVD_VARIANT_TMA) {
     // batches: the TMA ring must wait for each store's completion before
     // crediting it, which costs ~30% of its throughput; the full-grid LSU

@@ -41,6 +41,7 @@ def main():
     ap.add_argument("--runs", default="1,2,4,8,16,32,64")
     ap.add_argument("--tokens", type=int, default=8192)
     ap.add_argument("--no-nccl", action="store_true")
+    ap.add_argument("--variant", default="", help="force lsu|lsu32|tma (default: library auto)")
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     dev = int(os.environ.get("LOCAL_RANK", 0))
@@ -67,6 +68,8 @@ def main():
                 dst = cache if me.role == "decode" else None
                 blob = cluster.peer_blob(me, cluster.exchange_blobs(src.export() if src else None, gloo))
                 peer = dst.open_peer(blob) if dst else None
+                if peer and a.variant:
+                    peer.set(kvd.OPT_VARIANT, {"lsu": 1, "lsu32": 2, "tma": 4}[a.variant])
                 res = {}
                 for label, coalesce in (("pull", 1), ("pull_nocoalesce", 0)):
                     t_dev = 0.0
@@ -91,7 +94,7 @@ def main():
                         dist.barrier(group=gloo)
                         info = {}
                     res[label] = {"t": t_dev, "runs": info.get("runs"), "variant": info.get("variant"),
-                                  "ctas": info.get("ctas")}
+                                  "ctas": info.get("ctas"), "threads": info.get("threads")}
                 span = cache.span_bytes
                 per = n * NL * 2 * span
 
@@ -120,6 +123,7 @@ def main():
                         out[label + "_gbs_per_pair"] = round(per * a.iters / t / 1e9, 1)
                         out[label + "_runs"] = dec[0]["res"][label]["runs"]
                     out["variant"] = dec[0]["res"]["pull"]["variant"]
+                    out["threads"] = dec[0]["res"]["pull"].get("threads")
                     out["ctas"] = dec[0]["res"]["pull"]["ctas"]
                     if not a.no_nccl:
                         rs = [s["base"]["n1_gather_send_recv_scatter"] for s in dec]
