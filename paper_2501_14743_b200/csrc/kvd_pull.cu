@@ -52,25 +52,36 @@ struct PullParams {
 struct alignas(16) V16 { uint32_t x, y, z, w; };
 struct alignas(32) V32 { uint32_t v[8]; };
 
+// Cache qualifiers, A/B-tested with tools/build_ab.sh (profiles/r01_ab_cache_hints.txt):
+// streaming ".cs" (evict-first) loads and stores beat ".nc.L1::no_allocate"
+// loads + plain stores by ~1 % in loopback and ~0.5 % over NVLink -- every
+// byte is touched exactly once, so nothing is worth keeping in L1/L2.
+#ifndef KVD_LD_Q
+#define KVD_LD_Q "ld.global.cs"
+#endif
+#ifndef KVD_ST_Q
+#define KVD_ST_Q "st.global.cs"
+#endif
+
 __device__ __forceinline__ V16 ld_peer(const V16* p) {
   V16 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+  asm volatile(KVD_LD_Q ".v4.u32 {%0,%1,%2,%3}, [%4];"
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
   return r;
 }
 __device__ __forceinline__ void st_local(V16* p, const V16& v) {
-  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};"
+  asm volatile(KVD_ST_Q ".v4.u32 [%0], {%1,%2,%3,%4};"
                :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
 __device__ __forceinline__ V32 ld_peer(const V32* p) {
   V32 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+  asm volatile(KVD_LD_Q ".v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=r"(r.v[0]), "=r"(r.v[1]), "=r"(r.v[2]), "=r"(r.v[3]),
                  "=r"(r.v[4]), "=r"(r.v[5]), "=r"(r.v[6]), "=r"(r.v[7]) : "l"(p));
   return r;
 }
 __device__ __forceinline__ void st_local(V32* p, const V32& v) {
-  asm volatile("st.global.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+  asm volatile(KVD_ST_Q ".v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
                :: "l"(p), "r"(v.v[0]), "r"(v.v[1]), "r"(v.v[2]), "r"(v.v[3]),
                   "r"(v.v[4]), "r"(v.v[5]), "r"(v.v[6]), "r"(v.v[7]) : "memory");
 }

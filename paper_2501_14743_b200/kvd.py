@@ -15,7 +15,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libkvd.so")
+LIB_PATH = os.environ.get("KVD_LIB_PATH") or os.path.join(_HERE, "libkvd.so")   # override: A/B builds
 
 OK, EINVAL, ERANGE, ELAYOUT, EHANDLE, ECUDA, ENOMEM, EBUSY, ESTATE = 0, -1, -2, -3, -4, -5, -6, -7, -8
 FP16, BF16, FP8, FP32 = 0, 1, 2, 3
