@@ -130,8 +130,11 @@ typedef enum {
   KVD_OPT_VARIANT = 3,      /* kvd_variant */
   KVD_OPT_THREADS = 4,      /* threads per CTA: multiple of 32; LSU 32..512 (default 512);
                                TMA: threads/32 pipes per CTA, 32..256 (default 96) */
-  KVD_OPT_STAGES = 5        /* TMA ring depth per pipe, 2..8 (default 4); pipes * stages *
+  KVD_OPT_STAGES = 5,       /* TMA ring depth per pipe, 2..8 (default 4); pipes * stages *
                                tile_bytes must fit in 225 KiB of shared memory */
+  KVD_OPT_AUDIT = 6         /* 1: every tile checks that it stays inside its layer tensors on
+                               both sides; violations are counted (kvd_peer_audit) and not
+                               copied.  A test/debug mode; 0 (default) off */
 } kvd_option;
 
 typedef struct kvd_cache_s* kvd_cache;
@@ -278,6 +281,10 @@ KVD_API kvd_status kvd_push(kvd_peer peer, uint64_t request_id, const int32_t* s
 
 /* Spin on kvd_poll_done until done or `timeout_us` elapses (KVD_EBUSY). */
 KVD_API kvd_status kvd_wait_done(kvd_peer peer, uint64_t request_id, int64_t timeout_us);
+
+/* Bounds-audit violations counted on this peer since KVD_OPT_AUDIT was set
+ * (synchronises the local device first).  KVD_ESTATE if auditing is off. */
+KVD_API kvd_status kvd_peer_audit(kvd_peer peer, uint64_t* violations);
 
 /* Describe the most recent kvd_pull on this peer. */
 KVD_API kvd_status kvd_last_pull_info(kvd_peer peer, kvd_pull_info* out);

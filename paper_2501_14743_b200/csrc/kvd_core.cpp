@@ -436,6 +436,7 @@ struct kvd_peer_s {
   std::vector<int4> runs4;
   kvd_pull_info last{};
   bool closed = false;
+  unsigned int* audit_ctr = nullptr;        // KVD_OPT_AUDIT violation counter (device)
   // §8 f4 head-sliced peer (row_bytes > 0): remote unit = block_size rows
   uint32_t row_bytes = 0;
   uint32_t dst_row_stride = 0;
@@ -688,6 +689,7 @@ static void peer_release(kvd_peer p) {
   if (p->flags) cudaFreeHost(p->flags);
   if (p->counters) cudaFree(p->counters);
   if (p->bytectr) cudaFree(p->bytectr);
+  if (p->audit_ctr) cudaFree(p->audit_ctr);
   for (auto& b : p->batch_bufs) {
     if (b.dev) cudaFree(b.dev);
     if (b.host) cudaFreeHost(b.host);
@@ -858,6 +860,20 @@ kvd_status kvd_peer_set(kvd_peer p, int option, int64_t value) {
       p->stages = (uint32_t)value;
       p->stages_set = true;
       return KVD_OK;
+    case KVD_OPT_AUDIT: {
+      DeviceGuard dg(p->local->device);
+      if (!dg.ok) return fail(KVD_ECUDA, "cannot select device %d", p->local->device);
+      if (value && !p->audit_ctr) {
+        KVD_CUDA(cudaMalloc(&p->audit_ctr, sizeof(unsigned int)));
+        KVD_CUDA(cudaMemset(p->audit_ctr, 0, sizeof(unsigned int)));
+        KVD_CUDA(cudaDeviceSynchronize());
+      } else if (!value && p->audit_ctr) {
+        KVD_CUDA(cudaDeviceSynchronize());
+        cudaFree(p->audit_ctr);
+        p->audit_ctr = nullptr;
+      }
+      return KVD_OK;
+    }
   }
   return fail(KVD_EINVAL, "unknown option %d", option);
 }
@@ -1017,6 +1033,9 @@ static kvd_status transfer(kvd_peer p, uint64_t request_id, const int32_t* src_i
   a.flag = p->flags_dev + slot;
   a.token = token;
   a.remote_stores = push ? 1u : 0u;
+  a.audit = p->audit_ctr;
+  a.src_layer_bytes = sg.layer_bytes;
+  a.dst_layer_bytes = dg_.layer_bytes;
 
   DeviceGuard dgd(p->local->device);
   if (!dgd.ok) return fail(KVD_ECUDA, "cannot select device %d", p->local->device);
@@ -1209,6 +1228,9 @@ kvd_status kvd_pull_batch(kvd_peer p, uint32_t num_requests, const uint64_t* req
   a.flags = p->flags_dev;
   a.counter = nullptr;                  // per-request completion replaces the CTA arrival
   a.remote_stores = 0;
+  a.audit = p->audit_ctr;
+  a.src_layer_bytes = sg.layer_bytes;
+  a.dst_layer_bytes = dg_.layer_bytes;
   uint32_t threads = 0, ctas = 0;
   s = launch_shape(p, pol, a, (uint64_t)n * per_entry, &threads, &ctas);
   if (s != KVD_OK) return s;
@@ -1269,6 +1291,19 @@ kvd_status kvd_wait_done(kvd_peer p, uint64_t request_id, int64_t timeout_us) {
       return fail(KVD_EBUSY, "request %llu not done after %lld us", (unsigned long long)request_id,
                   (long long)timeout_us);
   }
+}
+
+kvd_status kvd_peer_audit(kvd_peer p, uint64_t* violations) {
+  if (!p || !violations) return fail(KVD_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lk(p->mu);
+  if (!p->audit_ctr) return fail(KVD_ESTATE, "auditing is off (set KVD_OPT_AUDIT)");
+  DeviceGuard dg(p->local->device);
+  if (!dg.ok) return fail(KVD_ECUDA, "cannot select device %d", p->local->device);
+  KVD_CUDA(cudaDeviceSynchronize());
+  unsigned int v = 0;
+  KVD_CUDA(cudaMemcpy(&v, p->audit_ctr, sizeof(v), cudaMemcpyDeviceToHost));
+  *violations = v;
+  return KVD_OK;
 }
 
 kvd_status kvd_last_pull_info(kvd_peer p, kvd_pull_info* out) {

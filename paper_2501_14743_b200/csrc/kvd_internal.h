@@ -43,6 +43,11 @@ struct PullArgs {
   unsigned int remote_stores;       // 1: stores target a peer GPU (push) -> system-scope fences
   unsigned int smem_runs;           // 1: the kernel copies the run table into shared memory
                                     //    (set by launch_pull when it fits)
+  // Bounds audit (KVD_OPT_AUDIT; compute-sanitizer is closed on this pool):
+  // when non-null every tile checks that its source and destination bytes
+  // lie inside their layer tensors, counts violations here and skips them.
+  unsigned int* audit;
+  unsigned long long src_layer_bytes, dst_layer_bytes;
 
   // TP-resharding (§8 f4): row_bytes > 0 makes every unit block_size rows
   // of row_bytes, src_row_stride / dst_row_stride apart, and shifts the

@@ -46,8 +46,8 @@ struct PullParams {
 };
 
 // ---------------------------------------------------------------------------
-// vector load/store: peer loads go through the non-coherent path without
-// allocating in L1 (each byte is read exactly once); stores are plain.
+// vector load/store through integer registers; streaming cache qualifiers
+// (each byte is read and written exactly once).
 // ---------------------------------------------------------------------------
 struct alignas(16) V16 { uint32_t x, y, z, w; };
 struct alignas(32) V32 { uint32_t v[8]; };
@@ -152,6 +152,7 @@ struct Tile {
   unsigned int bytes;
   unsigned int run;
   unsigned long long off;
+  unsigned int skip;       // bounds audit: counted violation, do not copy
 };
 
 // Tile t -> addresses.  Segments are (layer, plane, run); a tile never
@@ -205,7 +206,42 @@ __device__ __forceinline__ Tile tile_at(const PullArgs& a, const int4* runs, uns
   T.bytes = avail < a.tile_bytes ? (unsigned int)avail : a.tile_bytes;
   T.run = (unsigned int)lo;
   T.off = in_run;
+  T.skip = 0;
   return T;
+}
+
+// Bounds audit: the bytes a tile touches must lie inside layer l's tensor on
+// both sides.  Head-slice tiles span (rows-1) row strides plus one row.
+// Scalars only (no Tile address taken), so the hot loop keeps no stack frame.
+__device__ __noinline__ bool in_bounds(const PullArgs& a, unsigned long long s,
+                                       unsigned long long d, unsigned int bytes, unsigned int t) {
+  unsigned int l;
+  if (a.run_major) {
+    // recover the layer from the tile's source address (run-major order)
+    l = 0;
+    for (unsigned int k = 0; k < a.num_layers; ++k) {
+      const unsigned long long b = layer_base(a.src, k);
+      if (s >= b && s < b + a.src_layer_bytes) {
+        l = k;
+        break;
+      }
+    }
+  } else {
+    const unsigned int lp = t / a.tiles_per_lp;
+    l = (a.planes == 2) ? (lp >> 1) : lp;
+  }
+  unsigned long long src_ext = bytes, dst_ext = bytes;
+  if (a.row_bytes) {
+    const unsigned long long rows = bytes / a.row_bytes;
+    src_ext = (rows - 1) * a.src_row_stride + a.row_bytes;
+    dst_ext = (rows - 1) * a.dst_row_stride + a.row_bytes;
+  }
+  const unsigned long long s0 = layer_base(a.src, l), d0 = layer_base(a.dst, l);
+  return bytes > 0 && s >= s0 && s + src_ext <= s0 + a.src_layer_bytes && d >= d0 &&
+         d + dst_ext <= d0 + a.dst_layer_bytes && (s % 16) == 0 && (d % 16) == 0;
+}
+__device__ __forceinline__ bool tile_in_bounds(const PullArgs& a, const Tile& T, unsigned int t) {
+  return in_bounds(a, (unsigned long long)T.src, (unsigned long long)T.dst, T.bytes, t);
 }
 
 // --- batched drain (f1): per-request completion inside one launch ----------
@@ -340,11 +376,14 @@ pull_kernel(const __grid_constant__ PullParams<MAXR> P) {
   for (unsigned int t = blockIdx.x * warps_per_cta + (threadIdx.x >> 5); t < a.total_tiles;
        t += nwarps) {
     const Tile T = tile_at(a, runs, t);
-    if (GENERAL && a.row_bytes)
+    if (a.audit && !tile_in_bounds(a, T, t)) {           // bounds audit: count, skip
+      if (lane == 0) atomicAdd(a.audit, 1u);
+    } else if (GENERAL && a.row_bytes) {
       warp_copy_rows<V, U>(T.dst, T.src, T.bytes, lane, a.row_bytes, a.src_row_stride,
                            a.dst_row_stride);
-    else
+    } else {
       warp_copy<V, U>(T.dst, T.src, T.bytes, lane);
+    }
     if (GENERAL && a.nreqs) credit_tile(a, T, cr, lane == 0, true);   // batched drain
   }
   if (GENERAL && a.nreqs) credit_flush(a, cr, lane == 0, true);
@@ -364,9 +403,10 @@ __device__ __forceinline__ void tma_load(void* smem, const void* gsrc, unsigned 
                                          uint64_t* bar) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
                :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
-  asm volatile(
-      "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-      :: "r"(smem_u32(smem)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+  if (bytes)   // a 0-byte (audited-out) tile completes the phase with the arrive alone
+    asm volatile(
+        "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        :: "r"(smem_u32(smem)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
@@ -378,9 +418,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "}\n" :: "r"(smem_u32(bar)), "r"(parity) : "memory");
 }
 __device__ __forceinline__ void tma_store(void* gdst, const void* smem, unsigned int bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
-               :: "l"(gdst), "r"(smem_u32(smem)), "r"(bytes) : "memory");
-  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  if (bytes)
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                 :: "l"(gdst), "r"(smem_u32(smem)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");   // (possibly empty) group
+}
+
+// Bounds audit for the TMA ring: a tile outside its layer tensors is counted
+// and skipped (0-byte load/store) so the ring's bookkeeping stays intact.
+__device__ __forceinline__ Tile audited(const PullArgs& a, Tile T, unsigned int t) {
+  if (a.audit && !tile_in_bounds(a, T, t)) {
+    atomicAdd(a.audit, 1u);
+    T.skip = 1;
+  }
+  return T;
 }
 __device__ __forceinline__ void tma_wait_read_1() {
   asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
@@ -429,13 +480,14 @@ pull_kernel_tma(const __grid_constant__ PullParams<MAXR> P, unsigned int stages)
     Tile pend[kCreditLag + 1];
     Credit cr;
     for (unsigned int k = 0; k < S && k < count; ++k) {
-      tiles[k] = tile_at(a, runs, pipe + k * npipes);
-      tma_load(ring + (size_t)k * a.tile_bytes, tiles[k].src, tiles[k].bytes, &bar[k]);
+      tiles[k] = audited(a, tile_at(a, runs, pipe + k * npipes), pipe + k * npipes);
+      tma_load(ring + (size_t)k * a.tile_bytes, tiles[k].src, tiles[k].skip ? 0u : tiles[k].bytes,
+               &bar[k]);
     }
     for (unsigned int i = 0; i < count; ++i) {
       const unsigned int s = i % S;
       mbar_wait(&bar[s], (i / S) & 1u);
-      tma_store(tiles[s].dst, ring + (size_t)s * a.tile_bytes, tiles[s].bytes);
+      tma_store(tiles[s].dst, ring + (size_t)s * a.tile_bytes, tiles[s].skip ? 0u : tiles[s].bytes);
       if (a.nreqs) pend[i % (kCreditLag + 1)] = tiles[s];
       if (i >= 1) {
         const unsigned int sp = (i - 1) % S;
@@ -443,8 +495,9 @@ pull_kernel_tma(const __grid_constant__ PullParams<MAXR> P, unsigned int stages)
         // refill the stage of tile i-1 with tile i-1+S
         const unsigned int k = i - 1 + S;
         if (k < count) {
-          tiles[sp] = tile_at(a, runs, pipe + k * npipes);
-          tma_load(ring + (size_t)sp * a.tile_bytes, tiles[sp].src, tiles[sp].bytes, &bar[sp]);
+          tiles[sp] = audited(a, tile_at(a, runs, pipe + k * npipes), pipe + k * npipes);
+          tma_load(ring + (size_t)sp * a.tile_bytes, tiles[sp].src,
+                   tiles[sp].skip ? 0u : tiles[sp].bytes, &bar[sp]);
         }
       }
       if (a.nreqs && i >= kCreditLag) {

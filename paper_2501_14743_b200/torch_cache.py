@@ -101,6 +101,10 @@ class Peer:
     def wait(self, request_id: int, timeout_us: int = 30_000_000) -> None:
         kvd.kvd_wait_done(self.handle, request_id, timeout_us)
 
+    def audit(self) -> int:
+        """Bounds-audit violations (KVD_OPT_AUDIT must be set)."""
+        return kvd.kvd_peer_audit(self.handle)
+
     def info(self) -> dict:
         return kvd.kvd_last_pull_info(self.handle).as_dict()
 
