@@ -132,9 +132,11 @@ typedef enum {
                                TMA: threads/32 pipes per CTA, 32..256 (default 96) */
   KVD_OPT_STAGES = 5,       /* TMA ring depth per pipe, 2..8 (default 4); pipes * stages *
                                tile_bytes must fit in 225 KiB of shared memory */
-  KVD_OPT_AUDIT = 6         /* 1: every tile checks that it stays inside its layer tensors on
+  KVD_OPT_AUDIT = 6,        /* 1: every tile checks that it stays inside its layer tensors on
                                both sides; violations are counted (kvd_peer_audit) and not
                                copied.  A test/debug mode; 0 (default) off */
+  KVD_OPT_TIMING = 7        /* 1: record CUDA events right around every pull kernel on the
+                               caller's stream; kvd_peer_kernel_time sums them.  0 (default) off */
 } kvd_option;
 
 typedef struct kvd_cache_s* kvd_cache;
@@ -285,6 +287,11 @@ KVD_API kvd_status kvd_wait_done(kvd_peer peer, uint64_t request_id, int64_t tim
 /* Bounds-audit violations counted on this peer since KVD_OPT_AUDIT was set
  * (synchronises the local device first).  KVD_ESTATE if auditing is off. */
 KVD_API kvd_status kvd_peer_audit(kvd_peer peer, uint64_t* violations);
+
+/* Kernel-only device time of the launches recorded since the previous call
+ * (KVD_OPT_TIMING): waits for them, returns the summed milliseconds and the
+ * number of launches, and forgets them.  KVD_ESTATE if timing is off. */
+KVD_API kvd_status kvd_peer_kernel_time(kvd_peer peer, double* total_ms, uint64_t* launches);
 
 /* Describe the most recent kvd_pull on this peer. */
 KVD_API kvd_status kvd_last_pull_info(kvd_peer peer, kvd_pull_info* out);

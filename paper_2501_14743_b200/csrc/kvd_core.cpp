@@ -437,6 +437,8 @@ struct kvd_peer_s {
   kvd_pull_info last{};
   bool closed = false;
   unsigned int* audit_ctr = nullptr;        // KVD_OPT_AUDIT violation counter (device)
+  bool timing = false;                      // KVD_OPT_TIMING
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed, event_pool;
   // §8 f4 head-sliced peer (row_bytes > 0): remote unit = block_size rows
   uint32_t row_bytes = 0;
   uint32_t dst_row_stride = 0;
@@ -690,6 +692,11 @@ static void peer_release(kvd_peer p) {
   if (p->counters) cudaFree(p->counters);
   if (p->bytectr) cudaFree(p->bytectr);
   if (p->audit_ctr) cudaFree(p->audit_ctr);
+  for (auto* v : {&p->timed, &p->event_pool})
+    for (auto& ev : *v) {
+      cudaEventDestroy(ev.first);
+      cudaEventDestroy(ev.second);
+    }
   for (auto& b : p->batch_bufs) {
     if (b.dev) cudaFree(b.dev);
     if (b.host) cudaFreeHost(b.host);
@@ -860,6 +867,9 @@ kvd_status kvd_peer_set(kvd_peer p, int option, int64_t value) {
       p->stages = (uint32_t)value;
       p->stages_set = true;
       return KVD_OK;
+    case KVD_OPT_TIMING:
+      p->timing = value != 0;
+      return KVD_OK;
     case KVD_OPT_AUDIT: {
       DeviceGuard dg(p->local->device);
       if (!dg.ok) return fail(KVD_ECUDA, "cannot select device %d", p->local->device);
@@ -982,6 +992,24 @@ static void head_slice_plan(const kvd_peer_s* p, const kvd_geometry& sg, PairPla
   a.dst_unit_offset = p->head_offset_bytes;
 }
 
+// KVD_OPT_TIMING: CUDA events right around a pull kernel on its stream.
+static void timing_begin(kvd_peer_s* p, cudaStream_t s) {
+  if (!p->timing) return;
+  std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
+  if (!p->event_pool.empty()) {
+    ev = p->event_pool.back();
+    p->event_pool.pop_back();
+  } else if (cudaEventCreate(&ev.first) != cudaSuccess || cudaEventCreate(&ev.second) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  cudaEventRecord(ev.first, s);
+  p->timed.push_back(ev);
+}
+static void timing_end(kvd_peer_s* p, cudaStream_t s) {
+  if (p->timing && !p->timed.empty()) cudaEventRecord(p->timed.back().second, s);
+}
+
 // Pull (push = false): remote (imported) cache -> local cache, kernel on the
 // local GPU reading over NVLink.  Push (push = true, §8 f2): local cache ->
 // remote cache, kernel on the local GPU storing over NVLink.
@@ -1094,7 +1122,9 @@ static kvd_status transfer(kvd_peer p, uint64_t request_id, const int32_t* src_i
     uint32_t threads = 0, ctas = 0;
     s = launch_shape(p, pol, a, info.bytes, &threads, &ctas);
     if (s != KVD_OK) return s;
+    timing_begin(p, stream);
     e = kvd::launch_pull(a, p->runs4.data(), variant, ctas, threads, pol.stages, stream);
+    timing_end(p, stream);
     info.launches += 1;
     info.ctas = ctas;
     info.threads = threads;
@@ -1234,7 +1264,9 @@ kvd_status kvd_pull_batch(kvd_peer p, uint32_t num_requests, const uint64_t* req
   uint32_t threads = 0, ctas = 0;
   s = launch_shape(p, pol, a, (uint64_t)n * per_entry, &threads, &ctas);
   if (s != KVD_OK) return s;
+  timing_begin(p, stream);
   cudaError_t e = kvd::launch_pull(a, p->runs4.data(), pol.variant, ctas, threads, pol.stages, stream);
+  timing_end(p, stream);
   if (e != cudaSuccess) return cuda_fail(e, "batched pull launch");
   p->seq += num_requests;
   for (uint32_t q = 0; q < num_requests; ++q) {
@@ -1303,6 +1335,26 @@ kvd_status kvd_peer_audit(kvd_peer p, uint64_t* violations) {
   unsigned int v = 0;
   KVD_CUDA(cudaMemcpy(&v, p->audit_ctr, sizeof(v), cudaMemcpyDeviceToHost));
   *violations = v;
+  return KVD_OK;
+}
+
+kvd_status kvd_peer_kernel_time(kvd_peer p, double* total_ms, uint64_t* launches) {
+  if (!p || !total_ms || !launches) return fail(KVD_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lk(p->mu);
+  if (!p->timing) return fail(KVD_ESTATE, "timing is off (set KVD_OPT_TIMING)");
+  DeviceGuard dg(p->local->device);
+  if (!dg.ok) return fail(KVD_ECUDA, "cannot select device %d", p->local->device);
+  double sum = 0;
+  for (auto& ev : p->timed) {
+    KVD_CUDA(cudaEventSynchronize(ev.second));
+    float ms = 0;
+    KVD_CUDA(cudaEventElapsedTime(&ms, ev.first, ev.second));
+    sum += ms;
+  }
+  *total_ms = sum;
+  *launches = p->timed.size();
+  p->event_pool.insert(p->event_pool.end(), p->timed.begin(), p->timed.end());
+  p->timed.clear();
   return KVD_OK;
 }
 

@@ -21,14 +21,14 @@ OK, EINVAL, ERANGE, ELAYOUT, EHANDLE, ECUDA, ENOMEM, EBUSY, ESTATE = 0, -1, -2, 
 FP16, BF16, FP8, FP32 = 0, 1, 2, 3
 VARIANT_AUTO, VARIANT_LSU, VARIANT_LSU32, VARIANT_CE, VARIANT_TMA = 0, 1, 2, 3, 4
 OPT_MAX_CTAS, OPT_TILE_BYTES, OPT_COALESCE, OPT_VARIANT, OPT_THREADS, OPT_STAGES = 0, 1, 2, 3, 4, 5
-OPT_AUDIT = 6
+OPT_AUDIT, OPT_TIMING = 6, 7
 
 EXPORTED = (
     "kvd_layout_geometry", "kvd_plan", "kvd_blob_info", "kvd_register_cache",
     "kvd_unregister_cache", "kvd_export_handle", "kvd_open_peer", "kvd_open_peer_heads",
     "kvd_close_peer",
     "kvd_peer_set", "kvd_pull", "kvd_push", "kvd_pull_batch", "kvd_poll_done", "kvd_wait_done",
-    "kvd_last_pull_info", "kvd_peer_audit",
+    "kvd_last_pull_info", "kvd_peer_audit", "kvd_peer_kernel_time",
     "kvd_gather", "kvd_scatter", "kvd_strerror", "kvd_last_error", "kvd_abi_version",
 )
 
@@ -101,6 +101,7 @@ _SIGS = {
     "kvd_wait_done": [_p, _u64, _i64],
     "kvd_last_pull_info": [_p, ctypes.POINTER(kvd_pull_info)],
     "kvd_peer_audit": [_p, ctypes.POINTER(_u64)],
+    "kvd_peer_kernel_time": [_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_u64)],
     "kvd_gather": [_p, _pi32, _u32, _p, _p],
     "kvd_scatter": [_p, _pi32, _u32, _p, _p],
 }
@@ -301,6 +302,14 @@ def kvd_peer_audit(peer: int) -> int:
     v = _u64(0)
     _check(_lib.kvd_peer_audit(peer, ctypes.byref(v)), "kvd_peer_audit")
     return v.value
+
+
+def kvd_peer_kernel_time(peer: int):
+    """(summed kernel-only milliseconds, launches) since the previous call (KVD_OPT_TIMING)."""
+    ms, n = ctypes.c_double(0), _u64(0)
+    _check(_lib.kvd_peer_kernel_time(peer, ctypes.byref(ms), ctypes.byref(n)),
+           "kvd_peer_kernel_time")
+    return ms.value, n.value
 
 
 def kvd_last_pull_info(peer: int) -> kvd_pull_info:

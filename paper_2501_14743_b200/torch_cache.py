@@ -105,6 +105,10 @@ class Peer:
         """Bounds-audit violations (KVD_OPT_AUDIT must be set)."""
         return kvd.kvd_peer_audit(self.handle)
 
+    def kernel_time(self):
+        """(kernel-only ms summed, launches) since the last call; needs OPT_TIMING."""
+        return kvd.kvd_peer_kernel_time(self.handle)
+
     def info(self) -> dict:
         return kvd.kvd_last_pull_info(self.handle).as_dict()
 
