@@ -15,13 +15,18 @@ ranks [N/2, N) decode caches; decode rank N/2 + k pulls from prefill rank k
 A step = one pass of the per-request hot path over
 one batch of synthetic input on every pair: kvd_pull per request (validate +
 coalesce + one launch) -- or one kvd_pull_batch for the whole batch with
---batch (§8 f1) -- then kvd_poll_done until every request's device-side
+--batch (§8 f1) -- and kvd_poll_done until every request's device-side
 completion word flips.  C1/C2/C4: one request per pair per step; C3: the
 pair's 16 mixed-length requests.  Rows a1-a2 (register, export/open) are the
-paper's one-time Connect() and run before the timed region.
+paper's one-time Connect() and run before the timed region.  The K steps
+are issued back to back (a serving engine posts each pull as its request
+arrives) and completions retired as they land.
 `value` = bytes pulled by all pairs / device time of the K steps (CUDA events
 on the pull stream, max over ranks); `e2e` = the same bytes / host wall time
-from the first kvd_pull entry to the last completion observed.
+from the first kvd_pull entry to the last completion observed;
+`roofline.achieved` uses kernel-only time (library events right around each
+launch, KVD_OPT_TIMING); `p50_latency_ms` = issue -> completion observed of
+single requests on an idle pair, measured after the timed region.
 """
 from __future__ import annotations
 
@@ -406,11 +411,13 @@ def run_kvd(args, rank, world, local_rank):
     rid = [rank * 10_000_000]
     launches = [0]
 
-    def step(lat_out=None, evs=None):
-        """One pass of rows a3-a6 over this pair's requests.  `evs` brackets
-        the launches on the pull stream (the end event is recorded right
-        after the last launch, before the host starts polling)."""
-        ids, t_issue = [], []
+    pending = {}          # request id -> host issue time (ns)
+
+    def issue(evs=None):
+        """Rows a3-a4 for this pair's requests of one step: validate,
+        coalesce and launch (kvd_pull per request, or one kvd_pull_batch);
+        returns immediately ("post ... without block").  `evs`
+        brackets the step's launches on the pull stream."""
         if evs is not None:
             evs[0].record(stream)
         if args.batch:
@@ -418,27 +425,31 @@ def run_kvd(args, rank, world, local_rank):
             rid[0] += n_req
             t0 = time.perf_counter_ns()
             peer.pull_batch(ids, reqs, stream)
-            t_issue = [t0] * n_req
+            for i in ids:
+                pending[i] = t0
             launches[0] += 1
         else:
             for s, d in reqs:
                 rid[0] += 1
-                ids.append(rid[0])
-                t_issue.append(time.perf_counter_ns())
+                pending[rid[0]] = time.perf_counter_ns()
                 peer.pull(rid[0], s, d, stream)
                 launches[0] += 1
         if evs is not None:
             evs[1].record(stream)
-        pending = list(range(n_req))
-        while pending:
-            still = []
-            for q in pending:
-                if peer.poll(ids[q]):
+
+    def retire(until, lat_out=None):
+        """Row a6: poll completion words until at most `until` requests are
+        in flight."""
+        while len(pending) > until:
+            for i in list(pending):
+                if peer.poll(i):
+                    t0 = pending.pop(i)
                     if lat_out is not None:
-                        lat_out.append(time.perf_counter_ns() - t_issue[q])
-                else:
-                    still.append(q)
-            pending = still
+                        lat_out.append(time.perf_counter_ns() - t0)
+
+    def step(lat_out=None):
+        issue()
+        retire(0, lat_out)
 
     def barrier():
         torch.cuda.synchronize()
@@ -461,18 +472,31 @@ def run_kvd(args, rank, world, local_rank):
     if peer:
         peer.set(kvd.OPT_TIMING, 1)   # library-side events right around each pull kernel
     barrier()
+    # Throughput: the K steps are issued back to back, as a serving engine
+    # posts each request's pull when it arrives; completions are retired as
+    # they land (at most ~512 requests in flight, well under the 1024 slots).
     with sampler:
         wall0 = time.perf_counter()
         if peer:
             t_start.record(stream)
             for k in range(K):
-                step(lat_ns, ev[k])
+                issue(ev[k])
+                if len(pending) > 768:
+                    retire(512)
             t_end.record(stream)
+            retire(0)
         torch.cuda.synchronize()
         wall = time.perf_counter() - wall0
     barrier()
     timed_launches = launches[0]
     kern_ms_total, kern_launches = peer.kernel_time() if peer else (0.0, 0)
+    if peer:
+        peer.set(kvd.OPT_TIMING, 0)
+    # Per-request transfer latency (R16): issue -> completion observed, one
+    # step at a time on an otherwise idle pair, after the timed region.
+    if peer:
+        for _ in range(max(3, min(K, 50 if n_req == 1 else 5))):
+            step(lat_ns)
 
     info = peer.info() if peer else {}
     dev_s = t_start.elapsed_time(t_end) / 1e3 if peer else 0.0
