@@ -504,7 +504,7 @@ kvd_status tile_runs(const std::vector<kvd_run>& runs, const PairPlan& pp, uint3
 
 bool aligned32(const kvd::PullArgs& a, const std::vector<uint64_t>& src_bases,
                const std::vector<uint64_t>& dst_bases) {
-  if (a.unit_bytes % 32 || a.tile_bytes % 32) return false;
+  if (!a.unit_bytes || a.unit_bytes % 32 || a.tile_bytes % 32) return false;   // needs tile_runs first
   if (a.src.plane_stride % 32 || a.dst.plane_stride % 32) return false;
   if (a.src.block_stride % 32 || a.dst.block_stride % 32) return false;
   if (a.src.step % 32 || a.dst.step % 32 || a.src.base % 32 || a.dst.base % 32) return false;
@@ -513,9 +513,11 @@ bool aligned32(const kvd::PullArgs& a, const std::vector<uint64_t>& src_bases,
   return true;
 }
 
-uint32_t grid_for(uint64_t total_tiles, uint32_t threads, uint32_t max_ctas) {
-  const uint32_t wpc = threads / 32;
-  uint64_t need = (total_tiles + wpc - 1) / wpc;
+// tiles_per_warp: LSU chunks (kvd::lsu_tiles_per_warp()), TMA 1 (grid-stride pipes)
+uint32_t grid_for(uint64_t total_tiles, uint32_t threads, uint32_t max_ctas,
+                  uint32_t tiles_per_warp = 1) {
+  const uint64_t per_cta = (uint64_t)(threads / 32) * tiles_per_warp;
+  uint64_t need = (total_tiles + per_cta - 1) / per_cta;
   if (need < 1) need = 1;
   return (uint32_t)std::min<uint64_t>(need, max_ctas);
 }
@@ -919,7 +921,9 @@ static Policy choose_policy(const kvd_peer_s* p, uint64_t req_bytes, uint64_t av
   const bool over_link = p->remote_device != p->local->device;
   P.autov = p->variant == KVD_VARIANT_AUTO;
   P.small = P.autov && req_bytes <= (2ull << 20);
-  P.variant = P.autov ? ((over_link && !P.small) ? KVD_VARIANT_TMA : KVD_VARIANT_LSU) : p->variant;
+  // LSU32 (256-bit lanes) falls back to LSU when the layout is not 32 B aligned
+  P.variant = P.autov ? ((over_link && !P.small) ? KVD_VARIANT_TMA : KVD_VARIANT_LSU32)
+                      : p->variant;
   P.tma_defaults = P.variant == KVD_VARIANT_TMA && P.autov;
   P.tile = p->tile_set ? p->tile_bytes
                        : (P.tma_defaults ? 32768u : (P.small ? 2048u : p->tile_bytes));
@@ -965,13 +969,16 @@ static kvd_status launch_shape(const kvd_peer_s* p, Policy& P, const kvd::PullAr
       const uint64_t per_cta = (uint64_t)(threads / 32) * (P.stages - 1) * avg_tile;
       const uint64_t want = ((4608ull << 10) + per_cta - 1) / per_cta;
       max_ctas = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(want, 32), (uint64_t)p->sm_count);
-    } else {
+    } else if (P.variant == KVD_VARIANT_TMA) {
       const int per_sm = kvd::pull_ctas_per_sm(P.variant, threads, a.nruns);
       max_ctas = (uint32_t)(p->sm_count * per_sm);
+    } else {
+      max_ctas = 0x7fffffffu;   // LSU: one chunk per CTA, hardware schedules them in order
     }
   }
   *threads_out = threads;
-  *ctas_out = grid_for(a.total_tiles, threads, max_ctas);
+  *ctas_out = grid_for(a.total_tiles, threads, max_ctas,
+                       P.variant == KVD_VARIANT_TMA ? 1u : kvd::lsu_tiles_per_warp());
   return KVD_OK;
 }
 
@@ -1192,15 +1199,16 @@ kvd_status kvd_pull_batch(kvd_peer p, uint32_t num_requests, const uint64_t* req
     // batches: the TMA ring must wait for each store's completion before
     // crediting it, which costs ~30% of its throughput; the full-grid LSU
     // mover credits after a warp fence and stays at the link ceiling
-    pol.variant = KVD_VARIANT_LSU;
+    pol.variant = KVD_VARIANT_LSU32;
     pol.tma_defaults = false;
     pol.tile = p->tile_bytes;
   }
   if (p->row_bytes) head_slice_plan(p, sg, pp, pol, a);
-  if (pol.variant == KVD_VARIANT_LSU32 && !aligned32(a, p->src_bases, p->local->bases))
-    pol.variant = KVD_VARIANT_LSU;
   s = tile_runs(p->runs, pp, NL, pol.tile, p->runs4, a, /*run_major=*/true);
   if (s != KVD_OK) return s;
+  // after tile_runs: aligned32 inspects the unit and tile sizes it set
+  if (pol.variant == KVD_VARIANT_LSU32 && !aligned32(a, p->src_bases, p->local->bases))
+    pol.variant = KVD_VARIANT_LSU;
 
   // completion slots, one per request
   std::vector<uint32_t> slots;
@@ -1404,11 +1412,8 @@ static kvd_status gather_scatter(kvd_cache c, const int32_t* ids, uint32_t n, ui
   if (!dgd.ok) return fail(KVD_ECUDA, "cannot select device %d", c->device);
   if (a.nruns > kvd::max_param_runs())
     return fail(KVD_ERANGE, "baseline gather/scatter supports at most %u runs", kvd::max_param_runs());
-  int dev_sms = 148;
-  cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
   const uint32_t threads = 512;
-  const uint32_t ctas = grid_for(a.total_tiles, threads,
-                                 (uint32_t)(dev_sms * kvd::pull_ctas_per_sm(KVD_VARIANT_LSU, threads, a.nruns)));
+  const uint32_t ctas = grid_for(a.total_tiles, threads, 0x7fffffffu, kvd::lsu_tiles_per_warp());
   cudaError_t e = kvd::launch_pull(a, c->runs4.data(), KVD_VARIANT_LSU, ctas, threads, 0,
                                    (cudaStream_t)stream_);
   if (e != cudaSuccess) return cuda_fail(e, gather ? "gather launch" : "scatter launch");

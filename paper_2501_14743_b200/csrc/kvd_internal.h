@@ -80,6 +80,8 @@ enum Variant : int { kLsu16 = 1, kLsu32 = 2, kTma = 4 };
 unsigned int max_param_runs();
 // Deepest TMA ring (stages per pipe).
 unsigned int max_stages();
+// LSU mover: tiles each warp copies per CTA chunk (grid = tiles / (warps * this)).
+unsigned int lsu_tiles_per_warp();
 
 // Launch one pull kernel.  runs_host must hold args.nruns entries when
 // args.nruns <= max_param_runs(); otherwise args.runs_dev is used.
