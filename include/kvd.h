@@ -281,6 +281,21 @@ KVD_API kvd_status kvd_pull_batch(kvd_peer peer, uint32_t num_requests,
 KVD_API kvd_status kvd_push(kvd_peer peer, uint64_t request_id, const int32_t* src_ids,
                             const int32_t* dst_ids, uint32_t n, void* stream);
 
+/* Prefill side of Complete() ("When the prefill worker receives the
+ * Complete() message, it notifies the inference engine to release the KV
+ * cache block"; P:L375 the request ID is written into the prefill's memory
+ * one-sidedly).  Every pull from an exported cache, on completion, posts its
+ * request_id into a mailbox in the EXPORTER's device memory (a system-scope
+ * atomic claims a slot over NVLink, then a release store publishes it).
+ * Called on the exporter's cache, this copies up to `cap` newly completed
+ * request ids into `request_ids` (in completion order) and sets *n; the
+ * caller may then reuse those source blocks.  Each id is returned once.  The
+ * mailbox holds 4096 notifications: poll at least that often, else
+ * KVD_EBUSY reports lost notifications.  Synchronous (one small
+ * device-to-host copy); returns *n = 0 before the first export. */
+KVD_API kvd_status kvd_poll_released(kvd_cache exporter, uint64_t* request_ids, uint32_t cap,
+                                     uint32_t* n);
+
 /* Spin on kvd_poll_done until done or `timeout_us` elapses (KVD_EBUSY). */
 KVD_API kvd_status kvd_wait_done(kvd_peer peer, uint64_t request_id, int64_t timeout_us);
 

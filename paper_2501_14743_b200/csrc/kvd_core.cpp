@@ -205,7 +205,7 @@ struct Planner {
 // a2: blob codec (little-endian, fixed width)
 // ===========================================================================
 constexpr uint32_t kMagic = 0x4244564bu;  // "KVDB"
-constexpr uint32_t kBlobVersion = 1;
+constexpr uint32_t kBlobVersion = 2;
 
 struct BlobAlloc {
   cudaIpcMemHandle_t handle;
@@ -223,6 +223,8 @@ struct Blob {
   kvd_layout layout{};
   std::vector<BlobAlloc> allocs;
   std::vector<BlobLayer> layers;
+  bool has_mbox = false;          // release mailbox (Complete() -> prefill)
+  BlobAlloc mbox{};
 };
 
 struct Writer {
@@ -265,6 +267,12 @@ std::vector<uint8_t> encode_blob(const Blob& B) {
     w.u32(0);
     w.u64(l.offset);
   }
+  w.u32(B.has_mbox ? 1u : 0u);
+  if (B.has_mbox) {
+    w.raw(&B.mbox.handle, sizeof(B.mbox.handle));
+    w.u64(B.mbox.base);
+    w.u64(B.mbox.size);
+  }
   w.u32(kMagic);  // trailer
   return w.b;
 }
@@ -301,7 +309,16 @@ kvd_status decode_blob(const void* data, size_t len, Blob* B) {
     l.offset = r.u64();
     if (l.alloc >= na) return fail(KVD_EHANDLE, "blob: layer references allocation %u", l.alloc);
   }
+  const uint32_t has_mbox = r.u32();
+  if (has_mbox > 1) return fail(KVD_EHANDLE, "blob: bad mailbox flag");
+  B->has_mbox = has_mbox == 1;
+  if (B->has_mbox) {
+    r.raw(&B->mbox.handle, sizeof(B->mbox.handle));
+    B->mbox.base = r.u64();
+    B->mbox.size = r.u64();
+  }
   if (r.u32() != kMagic || !r.ok) return fail(KVD_EHANDLE, "blob: bad trailer");
+  if (r.i != len) return fail(KVD_EHANDLE, "blob: %zu trailing bytes", len - r.i);
   return KVD_OK;
 }
 
@@ -378,6 +395,10 @@ struct kvd_cache_s {
   std::vector<kvd_run> runs;
   std::vector<int4> runs4;
   std::vector<int32_t> iota;
+  // release mailbox (exporter side): importers post completed request ids
+  unsigned long long* mbox_dev = nullptr;
+  uint64_t mbox_head = 0;                 // next sequence to consume
+  std::vector<unsigned long long> mbox_host;
 };
 
 namespace {
@@ -390,6 +411,7 @@ struct kvd_peer_s {
   int remote_device = -1;
   bool same_process = false;
   std::vector<cudaIpcMemHandle_t> opened;  // handles we opened (to close)
+  unsigned long long* mbox = nullptr;       // the exporter's release mailbox, mapped here
   unsigned long long* d_src_bases = nullptr;
   std::vector<uint64_t> src_bases;         // host copy of the mapped remote layer bases
 
@@ -634,6 +656,7 @@ kvd_status kvd_unregister_cache(kvd_cache c) {
   {
     DeviceGuard dg(c->device);
     if (c->d_bases) cudaFree(c->d_bases);
+    if (c->mbox_dev) cudaFree(c->mbox_dev);
   }
   delete c;
   return KVD_OK;
@@ -675,6 +698,24 @@ kvd_status kvd_export_handle(kvd_cache c, void* blob, size_t* blob_len) {
       B.allocs.push_back(a);
     }
     B.layers.push_back(BlobLayer{it->second, c->bases[l] - abase});
+  }
+  {
+    // the release mailbox importers post completed request ids into
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (!c->mbox_dev) {
+      KVD_CUDA(cudaMalloc(&c->mbox_dev, kvd::kMailboxWords * sizeof(unsigned long long)));
+      KVD_CUDA(cudaMemset(c->mbox_dev, 0, kvd::kMailboxWords * sizeof(unsigned long long)));
+      KVD_CUDA(cudaDeviceSynchronize());
+      c->mbox_head = 0;
+    }
+    cudaError_t e = cudaIpcGetMemHandle(&B.mbox.handle, c->mbox_dev);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(KVD_EHANDLE, "cudaIpcGetMemHandle(mailbox): %s", cudaGetErrorString(e));
+    }
+    B.has_mbox = true;
+    B.mbox.base = (uint64_t)(uintptr_t)c->mbox_dev;
+    B.mbox.size = kvd::kMailboxWords * sizeof(unsigned long long);
   }
   std::vector<uint8_t> bytes = encode_blob(B);
   const size_t cap = *blob_len;
@@ -784,6 +825,19 @@ static kvd_status open_impl(kvd_cache local, const void* blob, size_t blob_len,
       if (s != KVD_OK) return s;
       p->opened.push_back(B.allocs[i].handle);
       alloc_va[i] = (uint64_t)(uintptr_t)ptr;
+    }
+  }
+  if (B.has_mbox) {
+    if (B.mbox.size < kvd::kMailboxWords * sizeof(unsigned long long))
+      return fail(KVD_EHANDLE, "blob: mailbox too small");
+    if (p->same_process) {
+      p->mbox = (unsigned long long*)(uintptr_t)B.mbox.base;
+    } else {
+      void* ptr = nullptr;
+      s = ipc_open(B.mbox.handle, local->device, &ptr);
+      if (s != KVD_OK) return s;
+      p->opened.push_back(B.mbox.handle);
+      p->mbox = (unsigned long long*)ptr;
     }
   }
   std::vector<uint64_t> src(B.layers.size());
@@ -1068,6 +1122,8 @@ static kvd_status transfer(kvd_peer p, uint64_t request_id, const int32_t* src_i
   a.flag = p->flags_dev + slot;
   a.token = token;
   a.remote_stores = push ? 1u : 0u;
+  a.request_id = request_id;
+  a.mbox = push ? nullptr : p->mbox;   // Complete() -> the prefill exporter (pull only)
   a.audit = p->audit_ctr;
   a.src_layer_bytes = sg.layer_bytes;
   a.dst_layer_bytes = dg_.layer_bytes;
@@ -1082,7 +1138,7 @@ static kvd_status transfer(kvd_peer p, uint64_t request_id, const int32_t* src_i
   info.bytes = (uint64_t)n * NL * 2 * sg.span_bytes;
   cudaError_t e = cudaSuccess;
   if (n == 0) {
-    e = kvd::launch_flag_only(a.flag, token, stream);
+    e = kvd::launch_flag_only(a.flag, token, a.mbox, request_id, stream);
     info.launches = 1;
     info.ctas = 1;
   } else if (variant == KVD_VARIANT_CE) {
@@ -1101,7 +1157,7 @@ static kvd_status transfer(kvd_peer p, uint64_t request_id, const int32_t* src_i
             ++launches;
           }
         }
-    if (e == cudaSuccess) e = kvd::launch_flag_only(a.flag, token, stream);
+    if (e == cudaSuccess) e = kvd::launch_flag_only(a.flag, token, a.mbox, request_id, stream);
     info.launches = launches + 1;
     info.segments = launches;
   } else {
@@ -1223,7 +1279,8 @@ kvd_status kvd_pull_batch(kvd_peer p, uint32_t num_requests, const uint64_t* req
   const size_t m = p->runs4.size();
   const size_t off_reqs = m * sizeof(int4);
   const size_t off_tok = off_reqs + num_requests * sizeof(uint4);
-  const size_t off_pos = off_tok + num_requests * sizeof(unsigned long long);
+  const size_t off_ids = off_tok + num_requests * sizeof(unsigned long long);
+  const size_t off_pos = off_ids + num_requests * sizeof(unsigned long long);
   const size_t bytes_needed = off_pos + std::max<size_t>(m, 1) * sizeof(uint32_t);
   int32_t bi = -1;
   for (size_t b = 0; b < p->batch_bufs.size(); ++b)
@@ -1248,6 +1305,7 @@ kvd_status kvd_pull_batch(kvd_peer p, uint32_t num_requests, const uint64_t* req
     memcpy(B.host + off_reqs + q * sizeof(uint4), &R, sizeof(uint4));
   }
   memcpy(B.host + off_tok, tokens.data(), num_requests * sizeof(uint64_t));
+  memcpy(B.host + off_ids, request_ids, num_requests * sizeof(uint64_t));
   {
     uint32_t pos = 0;
     for (size_t r = 0; r < m; ++r) {
@@ -1262,6 +1320,8 @@ kvd_status kvd_pull_batch(kvd_peer p, uint32_t num_requests, const uint64_t* req
   a.reqs = reinterpret_cast<const uint4*>(B.dev + off_reqs);
   a.tokens = reinterpret_cast<const unsigned long long*>(B.dev + off_tok);
   a.run_pos = reinterpret_cast<const unsigned int*>(B.dev + off_pos);
+  a.req_ids = reinterpret_cast<const unsigned long long*>(B.dev + off_ids);
+  a.mbox = p->mbox;
   a.bytectr = p->bytectr;
   a.flags = p->flags_dev;
   a.counter = nullptr;                  // per-request completion replaces the CTA arrival
@@ -1331,6 +1391,40 @@ kvd_status kvd_wait_done(kvd_peer p, uint64_t request_id, int64_t timeout_us) {
       return fail(KVD_EBUSY, "request %llu not done after %lld us", (unsigned long long)request_id,
                   (long long)timeout_us);
   }
+}
+
+kvd_status kvd_poll_released(kvd_cache c, uint64_t* request_ids, uint32_t cap, uint32_t* n) {
+  if (!c || !n || (cap && !request_ids)) return fail(KVD_EINVAL, "null argument");
+  *n = 0;
+  std::lock_guard<std::mutex> lk(c->mu);
+  if (!c->mbox_dev) return KVD_OK;               // never exported: nobody can complete
+  DeviceGuard dg(c->device);
+  if (!dg.ok) return fail(KVD_ECUDA, "cannot select device %d", c->device);
+  c->mbox_host.resize(kvd::kMailboxWords);
+  KVD_CUDA(cudaMemcpy(c->mbox_host.data(), c->mbox_dev,
+                      kvd::kMailboxWords * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  const unsigned long long* ring = c->mbox_host.data() + 8;
+  uint32_t k = 0;
+  while (k < cap) {
+    const uint64_t slot = c->mbox_head % kvd::kReleaseRing;
+    const unsigned long long seq = ring[2 * slot];
+    if (seq == c->mbox_head + 1) {
+      request_ids[k++] = ring[2 * slot + 1];
+      ++c->mbox_head;
+    } else if (seq > c->mbox_head + 1) {
+      // the ring wrapped before this reader caught up: entries were lost
+      const uint64_t lost = seq - (c->mbox_head + 1);
+      c->mbox_head = seq - 1;
+      *n = k;
+      return fail(KVD_EBUSY, "release mailbox overflowed: %llu notifications lost "
+                  "(poll at least every %u completions)", (unsigned long long)lost,
+                  kvd::kReleaseRing);
+    } else {
+      break;                                     // not yet written
+    }
+  }
+  *n = k;
+  return KVD_OK;
 }
 
 kvd_status kvd_peer_audit(kvd_peer p, uint64_t* violations) {

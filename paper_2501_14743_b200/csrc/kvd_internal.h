@@ -7,6 +7,13 @@
 
 namespace kvd {
 
+// Release mailbox (Complete() -> prefill, "sends the request ID to the
+// prefill worker"): device memory owned by the EXPORTER, IPC-mapped by every
+// importer.  u64 words: [0] tail (claimed with a system-scope atomic), [1..7]
+// padding, then kReleaseRing entries of {seq = slot + 1, request_id}.
+constexpr unsigned int kReleaseRing = 4096;
+constexpr size_t kMailboxWords = 8 + 2 * (size_t)kReleaseRing;
+
 // Where layer l of one side starts: table ? table[l] : base + l * step.
 // The peer's source side uses a device table of IPC-mapped prefill layer
 // bases; the baseline staging buffer uses the affine form.
@@ -39,6 +46,8 @@ struct PullArgs {
   unsigned int* counter;            // per-slot arrive counter (device, zero at launch)
   unsigned long long* flag;         // per-slot completion word (pinned, host-mapped)
   unsigned long long token;         // value stored to *flag when every byte has landed
+  unsigned long long request_id;    // posted to the exporter's release mailbox (if any)
+  unsigned long long* mbox;         // exporter's mailbox, mapped here (nullptr: none)
   const int4* runs_dev;             // run table in device memory when nruns > params capacity
   unsigned int remote_stores;       // 1: stores target a peer GPU (push) -> system-scope fences
   unsigned int smem_runs;           // 1: the kernel copies the run table into shared memory
@@ -70,6 +79,7 @@ struct PullArgs {
   const unsigned int* run_pos;      // [nruns] position of each run's first entry in the batch
   const uint4* reqs;                // [nreqs] {first entry, slot, total bytes lo, hi}
   const unsigned long long* tokens; // [nreqs]
+  const unsigned long long* req_ids;  // [nreqs] ids posted to the release mailbox
   unsigned long long* bytectr;      // per-slot byte counters (device, zero when idle)
   unsigned long long* flags;        // per-slot completion words (pinned, host-mapped)
 };
@@ -91,8 +101,10 @@ cudaError_t launch_pull(const PullArgs& args, const int4* runs_host, int variant
                         unsigned int ctas, unsigned int threads, unsigned int stages,
                         cudaStream_t stream);
 
-// Completion with no bytes (n = 0, or after copy-engine copies).
+// Completion with no bytes (n = 0, or after copy-engine copies); also posts
+// request_id to the exporter's release mailbox when mbox is non-null.
 cudaError_t launch_flag_only(unsigned long long* flag, unsigned long long token,
+                             unsigned long long* mbox, unsigned long long request_id,
                              cudaStream_t stream);
 
 // Resident CTAs per SM of the pull kernel for the given threads per CTA.

@@ -245,12 +245,27 @@ __device__ __forceinline__ bool tile_in_bounds(const PullArgs& a, const Tile& T,
   return in_bounds(a, (unsigned long long)T.src, (unsigned long long)T.dst, T.bytes, t);
 }
 
+// Complete() to the prefill side ("The completion transaction sends
+// the request ID to the prefill worker"; it then releases the
+// blocks): claim a slot of the exporter's mailbox with a system-scope atomic
+// over NVLink, write the id, then release the slot's sequence word.  Called
+// after every byte of the request has landed, i.e. after its last remote read.
+__device__ __forceinline__ void notify_release(const PullArgs& a, unsigned long long request_id) {
+  if (a.mbox == nullptr) return;
+  const unsigned long long s = atomicAdd_system(a.mbox, 1ull);
+  unsigned long long* e = a.mbox + 8 + 2 * (s % kReleaseRing);
+  *(volatile unsigned long long*)(e + 1) = request_id;
+  __threadfence_system();
+  st_release_sys(e, s + 1);
+}
+
 // --- batched drain (f1): per-request completion inside one launch ----------
 __device__ __forceinline__ void publish(const PullArgs& a, unsigned int q) {
   const uint4 R = a.reqs[q];
   a.bytectr[R.y] = 0ull;                 // slot idle again
   __threadfence_system();
   st_release_sys(&a.flags[R.y], a.tokens[q]);
+  notify_release(a, a.req_ids[q]);
 }
 
 // Credit `bytes` landed bytes to request q; the credit that reaches the
@@ -341,6 +356,7 @@ __device__ __forceinline__ void complete(const PullArgs& a) {
       *a.counter = 0u;
       __threadfence_system();
       st_release_sys(a.flag, a.token);
+      notify_release(a, a.request_id);
     }
   }
 }
@@ -523,9 +539,13 @@ pull_kernel_tma(const __grid_constant__ PullParams<MAXR> P, unsigned int stages)
   complete(a);
 }
 
-__global__ void flag_kernel(unsigned long long* flag, unsigned long long token) {
+__global__ void flag_kernel(unsigned long long* flag, unsigned long long token,
+                            unsigned long long* mbox, unsigned long long request_id) {
   __threadfence_system();
   st_release_sys(flag, token);
+  PullArgs a{};
+  a.mbox = mbox;
+  notify_release(a, request_id);
 }
 
 // ---------------------------------------------------------------------------
@@ -638,8 +658,9 @@ cudaError_t launch_pull(const PullArgs& args, const int4* runs_host, int variant
 }
 
 cudaError_t launch_flag_only(unsigned long long* flag, unsigned long long token,
+                             unsigned long long* mbox, unsigned long long request_id,
                              cudaStream_t stream) {
-  flag_kernel<<<1, 1, 0, stream>>>(flag, token);
+  flag_kernel<<<1, 1, 0, stream>>>(flag, token, mbox, request_id);
   return cudaGetLastError();
 }
 

@@ -28,7 +28,7 @@ EXPORTED = (
     "kvd_unregister_cache", "kvd_export_handle", "kvd_open_peer", "kvd_open_peer_heads",
     "kvd_close_peer",
     "kvd_peer_set", "kvd_pull", "kvd_push", "kvd_pull_batch", "kvd_poll_done", "kvd_wait_done",
-    "kvd_last_pull_info", "kvd_peer_audit", "kvd_peer_kernel_time",
+    "kvd_last_pull_info", "kvd_peer_audit", "kvd_peer_kernel_time", "kvd_poll_released",
     "kvd_gather", "kvd_scatter", "kvd_strerror", "kvd_last_error", "kvd_abi_version",
 )
 
@@ -101,6 +101,7 @@ _SIGS = {
     "kvd_wait_done": [_p, _u64, _i64],
     "kvd_last_pull_info": [_p, ctypes.POINTER(kvd_pull_info)],
     "kvd_peer_audit": [_p, ctypes.POINTER(_u64)],
+    "kvd_poll_released": [_p, _p, _u32, ctypes.POINTER(_u32)],
     "kvd_peer_kernel_time": [_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_u64)],
     "kvd_gather": [_p, _pi32, _u32, _p, _p],
     "kvd_scatter": [_p, _pi32, _u32, _p, _p],
@@ -295,6 +296,14 @@ def kvd_poll_done(peer: int, request_id: int) -> bool:
 
 def kvd_wait_done(peer: int, request_id: int, timeout_us: int = 10_000_000) -> None:
     _check(_lib.kvd_wait_done(peer, request_id, timeout_us), "kvd_wait_done")
+
+
+def kvd_poll_released(cache: int, cap: int = 4096) -> list:
+    """Exporter side of Complete(): request ids whose pulls completed since the last call."""
+    buf = np.zeros(max(1, cap), dtype=np.uint64)
+    n = _u32(0)
+    _check(_lib.kvd_poll_released(cache, _addr(buf), cap, ctypes.byref(n)), "kvd_poll_released")
+    return [int(x) for x in buf[:n.value]]
 
 
 def kvd_peer_audit(peer: int) -> int:

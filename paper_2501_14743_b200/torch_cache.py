@@ -54,6 +54,11 @@ class PagedCache:
     def open_peer(self, blob: bytes) -> "Peer":
         return Peer(self, kvd.kvd_open_peer(self.handle, blob))
 
+    def poll_released(self, cap: int = 4096) -> list:
+        """Exporter side of Complete(): ids of requests pulled from
+        this cache that have completed since the last call."""
+        return kvd.kvd_poll_released(self.handle, cap)
+
     def open_peer_heads(self, blob: bytes, head_offset: int) -> "Peer":
         """§8 f4: the blob's (fewer) heads land at heads [head_offset, ...)."""
         return Peer(self, kvd.kvd_open_peer_heads(self.handle, blob, head_offset))

@@ -17,7 +17,7 @@ MAGIC = 0x4244564B
 
 def make_blob(device, pid, layers=3, allocs=2, num_blocks=64):
     """A blob in the wire format of kvd_export_handle (test-side encoder)."""
-    b = struct.pack("<IIII", MAGIC, 1, device, 0)
+    b = struct.pack("<IIII", MAGIC, 2, device, 0)
     b += struct.pack("<QQ", pid, 0xABCDEF)
     b += struct.pack("<IIIIII", layers, 2, 64, 16, num_blocks, 0)   # layers, heads, dim, bs, nb, fp16
     sub = 16 * 2 * 64
@@ -29,6 +29,7 @@ def make_blob(device, pid, layers=3, allocs=2, num_blocks=64):
                                                layers * layer_bytes)
     for l in range(layers):
         b += struct.pack("<IIQ", l % allocs, 0, (l // allocs) * layer_bytes)
+    b += struct.pack("<I", 0)              # no release mailbox
     b += struct.pack("<I", MAGIC)
     return b
 
@@ -118,7 +119,7 @@ def test_synthesised_blob_round_trip_and_corruption():
     with pytest.raises(kvd.KvdError):
         kvd.kvd_blob_info(bytes(bad))
     bad = bytearray(blob)
-    off = len(blob) - 4 - 3 * 16                      # first layer's allocation index
+    off = len(blob) - 8 - 3 * 16                      # first layer's allocation index
     bad[off:off + 4] = struct.pack("<I", 7)
     with pytest.raises(kvd.KvdError):
         kvd.kvd_blob_info(bytes(bad))

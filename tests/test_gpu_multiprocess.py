@@ -20,7 +20,7 @@ def _geom():
     return kvdgen.CacheGeom(4, 8, 128, 16, 256, kvdgen.BF16)
 
 
-def _prefill(conn, dev, single_alloc):
+def _prefill(conn, dev, single_alloc, released):
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import torch
@@ -34,6 +34,8 @@ def _prefill(conn, dev, single_alloc):
     torch.cuda.synchronize()
     conn.send(c.export())
     conn.recv()          # decode finished: now the exporter may free its memory
+    # Complete() reached this process one-sidedly through the release mailbox
+    released.put(sorted(c.poll_released()))
     c.close()
 
 
@@ -82,7 +84,8 @@ def test_ipc_pull_across_processes(single_alloc):
     ctx = mp.get_context("spawn")
     a, b = ctx.Pipe()
     result = ctx.Queue()
-    p0 = ctx.Process(target=_prefill, args=(a, 0, single_alloc))
+    released = ctx.Queue()
+    p0 = ctx.Process(target=_prefill, args=(a, 0, single_alloc, released))
     p1 = ctx.Process(target=_decode, args=(b, 1, result))
     p0.start()
     p1.start()
@@ -90,3 +93,4 @@ def test_ipc_pull_across_processes(single_alloc):
     p0.join(60)
     assert p1.exitcode == 0 and p0.exitcode == 0
     assert result.get(timeout=5) is True
+    assert released.get(timeout=5) == [7000, 7001, 7002]

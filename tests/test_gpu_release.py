@@ -1,0 +1,105 @@
+"""Complete() toward the prefill side: every completed pull
+posts its request id into the exporter's release mailbox; the exporter's
+kvd_poll_released returns each id exactly once, after its bytes landed."""
+import numpy as np
+import pytest
+import torch
+
+import kvdgen
+from gpu_helpers import assert_layers_equal, make_pair, next_request_id, pull_and_wait
+from paper_2501_14743_b200 import kvd
+
+pytestmark = pytest.mark.gpu
+
+G = kvdgen.CacheGeom(2, 2, 64, 16, 256, kvdgen.FP16)
+
+
+def _exercise(pair):
+    ids = []
+    for k in range(3):                                    # single pulls
+        s, d = kvdgen.random_table(10 + k, 256, 256, seed=k)
+        rid = next_request_id()
+        pair.peer.pull(rid, s, d)
+        pair.peer.wait(rid)
+        ids.append(rid)
+    rid = next_request_id()                               # n = 0
+    pair.peer.pull(rid, [], [])
+    pair.peer.wait(rid)
+    ids.append(rid)
+    tables = kvdgen.disjoint_fragmented_tables([7, 0, 12], 256, 256, seed=9)
+    bids = [next_request_id() for _ in tables]            # batched drain
+    pair.peer.pull_batch(bids, tables)
+    for b in bids:
+        pair.peer.wait(b)
+    return ids + bids
+
+
+def test_release_mailbox_loopback():
+    pair = make_pair(G, G, seed=60)
+    try:
+        assert pair.src.poll_released() == []
+        ids = _exercise(pair)
+        torch.cuda.synchronize()
+        got = pair.src.poll_released()
+        assert sorted(got) == sorted(ids) and len(got) == len(set(got))
+        assert pair.src.poll_released() == []             # each id once
+        more = _exercise(pair)
+        got = []
+        for _ in range(100):
+            got += pair.src.poll_released(cap=3)          # small cap: resumes in order
+            if len(got) == len(more):
+                break
+        assert sorted(got) == sorted(more)
+    finally:
+        pair.close()
+
+
+def test_release_after_bytes_landed():
+    """The release id is posted only after the request's last read: once an
+    id is observed, the destination already holds every pulled byte."""
+    pair = make_pair(G, G, seed=61)
+    span = pair.src.span_bytes
+    src_view = [torch.from_numpy(h).view(2, 256, span) for h in pair.src_host]
+    try:
+        for it in range(200):
+            s, d = kvdgen.random_table(int(np.random.default_rng(it).integers(1, 40)), 256, 256,
+                                       seed=100 + it)
+            rid = next_request_id()
+            pair.peer.pull(rid, s, d)
+            got = []
+            while rid not in got:
+                got += pair.src.poll_released()
+            for l in range(G.num_layers):
+                now = pair.dst.layers[l].view(2, 256, span)[:, torch.from_numpy(d).long().cuda()].cpu()
+                assert torch.equal(now, src_view[l][:, torch.from_numpy(s).long()])
+            pair.peer.wait(rid)
+    finally:
+        pair.close()
+
+
+def test_push_does_not_post_releases():
+    pair = make_pair(G, G, seed=62)
+    try:
+        rev = pair.src.open_peer(pair.dst.export())
+        rid = next_request_id()
+        rev.push(rid, [1, 2], [3, 4])
+        rev.wait(rid)
+        torch.cuda.synchronize()
+        assert pair.dst.poll_released() == []
+        rev.close()
+    finally:
+        pair.close()
+
+
+@pytest.mark.gpu2
+def test_release_mailbox_two_gpus():
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs")
+    pair = make_pair(G, G, seed=63, src_dev=0, dst_dev=1)
+    try:
+        ids = _exercise(pair)
+        torch.cuda.synchronize(1)
+        got = pair.src.poll_released()
+        assert sorted(got) == sorted(ids)
+    finally:
+        pair.close()
