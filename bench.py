@@ -497,6 +497,26 @@ def run_kvd(args, rank, world, local_rank):
     if peer:
         for _ in range(max(3, min(K, 50 if n_req == 1 else 5))):
             step(lat_ns)
+    # Context: the copy engine over the same mapping (cudaMemcpyAsync per
+    # segment, KVD_VARIANT_CE) on a contiguous request of the same size.
+    ce_gbs = None
+    if peer and args.config != "c1":
+        n0 = min(n_blocks, g.num_blocks)
+        cs, cd = kvdgen.contiguous_table(n0, 0, g.num_blocks - n0)
+        peer.set(kvd.OPT_VARIANT, kvd.VARIANT_CE)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        rid[0] += 1
+        peer.pull(rid[0], cs, cd, stream)
+        peer.wait(rid[0])
+        e0.record(stream)
+        for _ in range(3):
+            rid[0] += 1
+            peer.pull(rid[0], cs, cd, stream)
+            peer.wait(rid[0])
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ce_gbs = 3 * n0 * g.num_layers * 2 * (src or dst).span_bytes / (e0.elapsed_time(e1) / 1e3) / 1e9
+        peer.set(kvd.OPT_VARIANT, {"lsu": 1, "lsu32": 2, "ce": 3, "tma": 4}.get(args.variant, 0))
 
     info = peer.info() if peer else {}
     dev_s = t_start.elapsed_time(t_end) / 1e3 if peer else 0.0
@@ -542,7 +562,7 @@ def run_kvd(args, rank, world, local_rank):
              "step_ms": float(np.mean(step_ms)) if step_ms else 0.0,
              "kern_ms": kern_ms_total / K if peer else 0.0, "kern_launches": kern_launches,
              "lat": lat_ns, "clock": sampler.summary(), "info": info, "base": base,
-             "launches": timed_launches, "runs": info.get("runs"),
+             "launches": timed_launches, "runs": info.get("runs"), "ce_gbs": ce_gbs,
              "bytes_per_step": bytes_per_step if peer else 0}
     all_stats = cluster.gather_stats(stats, gloo) if multi else [stats]
 
@@ -616,6 +636,11 @@ def run_kvd(args, rank, world, local_rank):
                     "what": "host wall from kvd_pull entry (host block-id tables -> kernel "
                             "parameters) to the host observing the pinned completion words"},
             "gpu_launches": sum(s["launches"] for s in dec),
+            "calibration": {
+                "copy_engine_gbs_per_pair": (round(float(np.mean([s["ce_gbs"] for s in dec])), 1)
+                                             if all(s["ce_gbs"] for s in dec) else None),
+                "what": "cudaMemcpyAsync per segment over the same mapping, contiguous request "
+                        "of the same size (context for the link ceiling; not the product path)"},
             "parity": bool(all(oks)),
             "clocks": clk,
         }

@@ -995,7 +995,7 @@ static Policy choose_policy(const kvd_peer_s* p, uint64_t req_bytes, uint64_t av
 }
 
 // Threads per CTA, TMA ring depth and grid size of a tiled launch.
-static kvd_status launch_shape(const kvd_peer_s* p, Policy& P, const kvd::PullArgs& a,
+static kvd_status launch_shape(const kvd_peer_s* p, Policy& P, kvd::PullArgs& a,
                                uint64_t bytes, uint32_t* threads_out, uint32_t* ctas_out) {
   const uint32_t threads =
       p->threads_set ? p->threads
@@ -1030,9 +1030,11 @@ static kvd_status launch_shape(const kvd_peer_s* p, Policy& P, const kvd::PullAr
       max_ctas = 0x7fffffffu;   // LSU: one chunk per CTA, hardware schedules them in order
     }
   }
+  // small requests: one tile per warp, so every tile is in flight at once
+  a.tiles_per_warp = P.small ? 1u : kvd::lsu_tiles_per_warp();
   *threads_out = threads;
   *ctas_out = grid_for(a.total_tiles, threads, max_ctas,
-                       P.variant == KVD_VARIANT_TMA ? 1u : kvd::lsu_tiles_per_warp());
+                       P.variant == KVD_VARIANT_TMA ? 1u : a.tiles_per_warp);
   return KVD_OK;
 }
 

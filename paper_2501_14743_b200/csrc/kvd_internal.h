@@ -50,6 +50,7 @@ struct PullArgs {
   unsigned long long* mbox;         // exporter's mailbox, mapped here (nullptr: none)
   const int4* runs_dev;             // run table in device memory when nruns > params capacity
   unsigned int remote_stores;       // 1: stores target a peer GPU (push) -> system-scope fences
+  unsigned int tiles_per_warp;      // LSU chunk = warps * this (host sets it; grid follows)
   unsigned int smem_runs;           // 1: the kernel copies the run table into shared memory
                                     //    (set by launch_pull when it fits)
   // Bounds audit (KVD_OPT_AUDIT; compute-sanitizer is closed on this pool):

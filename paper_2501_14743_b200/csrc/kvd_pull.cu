@@ -394,7 +394,7 @@ pull_kernel(const __grid_constant__ PullParams<MAXR> P) {
   // consecutive tiles.  With the default grid (one chunk per CTA) the GPU
   // sweeps the request front to back in launch order, which keeps DRAM
   // row locality: loopback 2970 -> 3330 GB/s vs a persistent grid-stride.
-  const unsigned int chunk = warps_per_cta * kTilesPerWarp;
+  const unsigned int chunk = warps_per_cta * (a.tiles_per_warp ? a.tiles_per_warp : kTilesPerWarp);
   for (unsigned int c0 = blockIdx.x * chunk; c0 < a.total_tiles; c0 += gridDim.x * chunk)
   for (unsigned int t = c0 + warp; t < c0 + chunk && t < a.total_tiles; t += warps_per_cta) {
     const Tile T = tile_at(a, runs, t);
