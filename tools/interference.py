@@ -77,8 +77,11 @@ def main():
     tg, _ = timed(lambda: gemms(KG), None)
     base_tflops = KG * flop / tg / 1e12
     out = {"gemm_alone_tflops": round(base_tflops, 1)}
-    for name, opts in (("tma", {kvd.OPT_VARIANT: kvd.VARIANT_TMA, kvd.OPT_THREADS: 32, kvd.OPT_STAGES: 6,
-                                kvd.OPT_TILE_BYTES: 32768, kvd.OPT_MAX_CTAS: 32}),
+    tma_ctas = [int(x) for x in os.environ.get("TMA_CTAS", "32").split(",")]
+    cfgs = [(f"tma{c}" if len(tma_ctas) > 1 else "tma",
+             {kvd.OPT_VARIANT: kvd.VARIANT_TMA, kvd.OPT_THREADS: 32, kvd.OPT_STAGES: 6,
+              kvd.OPT_TILE_BYTES: 32768, kvd.OPT_MAX_CTAS: c}) for c in tma_ctas]
+    for name, opts in (*cfgs,
                        ("lsu", {kvd.OPT_VARIANT: kvd.VARIANT_LSU32, kvd.OPT_THREADS: 512,
                                 kvd.OPT_TILE_BYTES: 16384, kvd.OPT_MAX_CTAS: 0}),
                        ("ce", {kvd.OPT_VARIANT: kvd.VARIANT_CE})):
