@@ -497,26 +497,6 @@ def run_kvd(args, rank, world, local_rank):
     if peer:
         for _ in range(max(3, min(K, 50 if n_req == 1 else 5))):
             step(lat_ns)
-    # Context: the copy engine over the same mapping (cudaMemcpyAsync per
-    # segment, KVD_VARIANT_CE) on a contiguous request of the same size.
-    ce_gbs = None
-    if peer and args.config != "c1":
-        n0 = min(n_blocks, g.num_blocks)
-        cs, cd = kvdgen.contiguous_table(n0, 0, g.num_blocks - n0)
-        peer.set(kvd.OPT_VARIANT, kvd.VARIANT_CE)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        rid[0] += 1
-        peer.pull(rid[0], cs, cd, stream)
-        peer.wait(rid[0])
-        e0.record(stream)
-        for _ in range(3):
-            rid[0] += 1
-            peer.pull(rid[0], cs, cd, stream)
-            peer.wait(rid[0])
-        e1.record(stream)
-        torch.cuda.synchronize()
-        ce_gbs = 3 * n0 * g.num_layers * 2 * (src or dst).span_bytes / (e0.elapsed_time(e1) / 1e3) / 1e9
-        peer.set(kvd.OPT_VARIANT, {"lsu": 1, "lsu32": 2, "ce": 3, "tma": 4}.get(args.variant, 0))
 
     info = peer.info() if peer else {}
     dev_s = t_start.elapsed_time(t_end) / 1e3 if peer else 0.0
@@ -552,6 +532,28 @@ def run_kvd(args, rank, world, local_rank):
     oks = [None] * world if multi else [ok]
     if multi:
         dist.all_gather_object(oks, bool(ok), group=gloo)
+
+    # Context (after the parity check, it overwrites destination blocks): the
+    # copy engine over the same mapping (cudaMemcpyAsync per segment,
+    # KVD_VARIANT_CE) on a contiguous request of the same size.
+    ce_gbs = None
+    if peer and args.config != "c1":
+        n0 = min(n_blocks, g.num_blocks)
+        cs, cd = kvdgen.contiguous_table(n0, 0, g.num_blocks - n0)
+        peer.set(kvd.OPT_VARIANT, kvd.VARIANT_CE)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        rid[0] += 1
+        peer.pull(rid[0], cs, cd, stream)
+        peer.wait(rid[0])
+        e0.record(stream)
+        for _ in range(3):
+            rid[0] += 1
+            peer.pull(rid[0], cs, cd, stream)
+            peer.wait(rid[0])
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ce_gbs = 3 * n0 * g.num_layers * 2 * span / (e0.elapsed_time(e1) / 1e3) / 1e9
+        peer.set(kvd.OPT_VARIANT, {"lsu": 1, "lsu32": 2, "ce": 3, "tma": 4}.get(args.variant, 0))
 
     base = {}
     if multi and not args.no_nccl:
