@@ -378,7 +378,7 @@ def run_kvd(args, rank, world, local_rank):
 
     def new_cache(seed):
         c = PagedCache(g.num_layers, g.num_kv_heads, g.head_dim, g.block_size, g.num_blocks,
-                       g.dtype, g.stride, dev)
+                       g.dtype, g.stride, dev, memory=args.memory)
         for l, t in enumerate(c.layers):
             kvdgen.torch_fill_random_(t, seed * 1000 + l)
         return c
@@ -624,10 +624,14 @@ def run_kvd(args, rank, world, local_rank):
                 "cache_dtype": "fp16" if g.dtype == kvdgen.FP16 else "bf16",
                 "variant": info0.get("variant"), "ctas": info0.get("ctas"),
                 "threads": info0.get("threads"), "tiles": info0.get("tiles"),
+                "memory": ("torch caching allocator (cudaMalloc; legacy IPC handles)"
+                           if args.memory == "torch" else
+                           "kvd_mem_alloc (CUDA VMM; POSIX-fd/fabric handles)"),
             },
             "gbs_per_pair": round(total / pairs / t_dev / 1e9, 2),
-            "frac_of_nvlink_900_per_pair": round(total / pairs / t_dev / 1e9 / NVLINK_NOMINAL_GBS,
-                                                 4),
+            # loopback never touches NVLink: no link fraction there
+            "frac_of_nvlink_900_per_pair": (round(total / pairs / t_dev / 1e9 /
+                                                  NVLINK_NOMINAL_GBS, 4) if multi else None),
             "p50_latency_ms": round(nearest_rank(lat_all, 50) / 1e6, 4),
             "p90_latency_ms": round(nearest_rank(lat_all, 90) / 1e6, 4),
             "step_device_ms": round(step_dev, 4),
@@ -700,6 +704,9 @@ def main():
     ap.add_argument("--threads", type=int, default=0)
     ap.add_argument("--max-ctas", type=int, default=0)
     ap.add_argument("--no-coalesce", action="store_true")
+    ap.add_argument("--memory", choices=["torch", "vmm"], default="torch",
+                    help="cache memory: torch/cudaMalloc (legacy IPC) or kvd_mem_alloc (VMM, "
+                         "POSIX-fd/fabric handles, §8 f3 groundwork)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-nccl", action="store_true", help="skip the NCCL send/recv baselines")
     args = ap.parse_args()

@@ -183,6 +183,39 @@ KVD_API kvd_status kvd_register_cache(int device, const kvd_layout* layout,
 KVD_API kvd_status kvd_unregister_cache(kvd_cache cache);
 
 /* ---------------------------------------------------------------------------
+ * §8 f3 groundwork: exportable cache memory (CUDA virtual memory management)
+ *
+ * The paper pulls across nodes.  With NVLink hardware the
+ * cross-node handle is a FABRIC handle of a VMM allocation (multi-node
+ * NVLink; needs an IMEX channel); inside one node the same allocation
+ * exports as a POSIX fd.  Caches placed in kvd_mem_alloc memory export such
+ * handles from kvd_export_handle automatically; the pull kernel is unchanged.
+ * ------------------------------------------------------------------------- */
+typedef enum {
+  KVD_MEM_AUTO = 0,      /* FABRIC when the driver permits it, else POSIX_FD */
+  KVD_MEM_POSIX_FD = 1,  /* intra-node: the importer fetches the exporter's fd
+                            with pidfd_getfd (Linux >= 5.6, same user, the
+                            exporter alive and in the importer's PID namespace) */
+  KVD_MEM_FABRIC = 8     /* multi-node NVLink: 64 B handle, importable on any
+                            node of the NVLink domain (IMEX) */
+} kvd_mem_kind;
+
+/* Allocate `bytes` (rounded up to the recommended granularity, 2 MiB on
+ * B200) of device memory on `device`, mapped read/write for that device.
+ * *size (may be NULL) = bytes reserved; *kind_out (may be NULL) = the kind
+ * obtained.  The caller owns the memory: free it with kvd_mem_free after
+ * every cache over it is unregistered and every importer has closed its
+ * peer.  Errors: KVD_EINVAL (null, zero size, unknown kind), KVD_ENOMEM,
+ * KVD_EHANDLE (kind not permitted here, e.g. FABRIC without IMEX),
+ * KVD_ECUDA. */
+KVD_API kvd_status kvd_mem_alloc(int device, uint64_t bytes, int kind, void** ptr,
+                                 uint64_t* size, int* kind_out);
+
+/* Free kvd_mem_alloc memory (synchronises its device first, like cudaFree).
+ * KVD_EINVAL if ptr is not the start of a kvd_mem_alloc allocation. */
+KVD_API kvd_status kvd_mem_free(void* ptr);
+
+/* ---------------------------------------------------------------------------
  * Row a2: one-time tensor-centric exchange (Connect())
  * ------------------------------------------------------------------------- */
 
@@ -191,8 +224,11 @@ KVD_API kvd_status kvd_unregister_cache(kvd_cache cache);
  * (allocation, offset) -- into the caller's buffer.  *blob_len: in =
  * capacity, out = bytes written (or needed, with KVD_ENOMEM).  The blob is
  * plain bytes; ship it to the decode process any way (torch.distributed,
- * TCPStore, socket).  Errors: KVD_EINVAL, KVD_ENOMEM, KVD_EHANDLE
- * (memory not legacy-IPC capable, e.g. VMM/expandable segments). */
+ * TCPStore, socket).  An allocation from kvd_mem_alloc is exported as its
+ * POSIX fd or fabric handle instead of a CUDA IPC handle (blob v3 records
+ * the kind per allocation).  Errors: KVD_EINVAL, KVD_ENOMEM, KVD_EHANDLE
+ * (memory neither cudaMalloc nor kvd_mem_alloc, e.g. torch expandable
+ * segments). */
 KVD_API kvd_status kvd_export_handle(kvd_cache cache, void* blob, size_t* blob_len);
 
 /* Import a peer cache's blob and bind it to a local cache.  For the pull

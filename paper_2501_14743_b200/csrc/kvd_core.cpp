@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "kvd_internal.h"
+#include "kvd_vmm.h"
 
 // ===========================================================================
 // errors
@@ -205,13 +206,22 @@ struct Planner {
 // a2: blob codec (little-endian, fixed width)
 // ===========================================================================
 constexpr uint32_t kMagic = 0x4244564bu;  // "KVDB"
-constexpr uint32_t kBlobVersion = 2;
+constexpr uint32_t kBlobVersion = 3;
 
+// One exported allocation: a legacy CUDA IPC handle (cudaMalloc memory) or a
+// VMM shareable handle (kvd_mem_alloc memory: POSIX fd or fabric, §8 f3).
 struct BlobAlloc {
-  cudaIpcMemHandle_t handle;
-  uint64_t base;     // exporter's virtual address (same-process import)
-  uint64_t size;
+  kvd::vmm::ExportRec rec;
+  uint64_t base = 0;  // exporter's virtual address (same-process import)
+  uint64_t size = 0;
 };
+static_assert(sizeof(cudaIpcMemHandle_t) == sizeof(kvd::vmm::ExportRec::payload),
+              "IPC handle must fit the export record payload");
+constexpr size_t kAllocRecBytes = 8 + sizeof(kvd::vmm::ExportRec::payload) + 16;
+
+bool known_kind(uint32_t k) {
+  return k == kvd::vmm::kLegacyIpc || k == kvd::vmm::kPosixFd || k == kvd::vmm::kFabric;
+}
 struct BlobLayer {
   uint32_t alloc;
   uint64_t offset;
@@ -257,22 +267,21 @@ std::vector<uint8_t> encode_blob(const Blob& B) {
   for (int k = 0; k < 5; ++k) w.u64((uint64_t)L.stride[k]);
   w.u32((uint32_t)B.allocs.size());
   w.u32((uint32_t)B.layers.size());
-  for (auto& a : B.allocs) {
-    w.raw(&a.handle, sizeof(a.handle));
+  auto put = [&w](const BlobAlloc& a) {
+    w.u32(a.rec.kind);
+    w.u32(a.rec.fd);
+    w.raw(a.rec.payload, sizeof(a.rec.payload));
     w.u64(a.base);
     w.u64(a.size);
-  }
+  };
+  for (auto& a : B.allocs) put(a);
   for (auto& l : B.layers) {
     w.u32(l.alloc);
     w.u32(0);
     w.u64(l.offset);
   }
   w.u32(B.has_mbox ? 1u : 0u);
-  if (B.has_mbox) {
-    w.raw(&B.mbox.handle, sizeof(B.mbox.handle));
-    w.u64(B.mbox.base);
-    w.u64(B.mbox.size);
-  }
+  if (B.has_mbox) put(B.mbox);
   w.u32(kMagic);  // trailer
   return w.b;
 }
@@ -294,14 +303,19 @@ kvd_status decode_blob(const void* data, size_t len, Blob* B) {
   if (!r.ok) return fail(KVD_EHANDLE, "blob: truncated header");
   if (nl != L.num_layers || na == 0 || na > nl)
     return fail(KVD_EHANDLE, "blob: inconsistent counts (%u allocations, %u layers)", na, nl);
-  if ((size_t)na * (sizeof(cudaIpcMemHandle_t) + 16) + (size_t)nl * 16 + 4 > len - r.i)
+  if ((size_t)na * kAllocRecBytes + (size_t)nl * 16 + 4 > len - r.i)
     return fail(KVD_EHANDLE, "blob: truncated body");
-  B->allocs.resize(na);
-  for (auto& a : B->allocs) {
-    r.raw(&a.handle, sizeof(a.handle));
+  auto get = [&r](BlobAlloc& a) {
+    a.rec.kind = r.u32();
+    a.rec.fd = r.u32();
+    r.raw(a.rec.payload, sizeof(a.rec.payload));
     a.base = r.u64();
     a.size = r.u64();
-  }
+    return known_kind(a.rec.kind);
+  };
+  B->allocs.resize(na);
+  for (auto& a : B->allocs)
+    if (!get(a)) return fail(KVD_EHANDLE, "blob: unknown handle kind %u", a.rec.kind);
   B->layers.resize(nl);
   for (auto& l : B->layers) {
     l.alloc = r.u32();
@@ -312,11 +326,8 @@ kvd_status decode_blob(const void* data, size_t len, Blob* B) {
   const uint32_t has_mbox = r.u32();
   if (has_mbox > 1) return fail(KVD_EHANDLE, "blob: bad mailbox flag");
   B->has_mbox = has_mbox == 1;
-  if (B->has_mbox) {
-    r.raw(&B->mbox.handle, sizeof(B->mbox.handle));
-    B->mbox.base = r.u64();
-    B->mbox.size = r.u64();
-  }
+  if (B->has_mbox && (!get(B->mbox) || B->mbox.rec.kind != kvd::vmm::kLegacyIpc))
+    return fail(KVD_EHANDLE, "blob: bad mailbox handle kind");
   if (r.u32() != kMagic || !r.ok) return fail(KVD_EHANDLE, "blob: bad trailer");
   if (r.i != len) return fail(KVD_EHANDLE, "blob: %zu trailing bytes", len - r.i);
   return KVD_OK;
@@ -340,18 +351,35 @@ PFN_memGetAddressRange get_address_range_fn() {
 }
 
 // ===========================================================================
-// IPC mapping registry: a handle may be opened once per device per process
+// mapping registry: an exported allocation is mapped once per device per
+// process (legacy IPC handles may not be opened twice; VMM imports share the VA)
 // ===========================================================================
 struct Mapping {
   void* ptr = nullptr;
   int refs = 0;
+  uint32_t kind = 0;
+  uint64_t size = 0;
 };
 std::mutex g_map_mu;
 std::map<std::pair<std::string, int>, Mapping> g_mappings;
 
-kvd_status ipc_open(const cudaIpcMemHandle_t& h, int device, void** out) {
+// Legacy handles are globally unique; a POSIX fd number is only unique inside
+// its exporter process and lifetime, so its key adds (pid, nonce, base, size).
+std::string map_key(const BlobAlloc& a, int64_t pid, uint64_t nonce) {
+  std::string k((const char*)&a.rec.kind, sizeof(a.rec.kind));
+  k.append((const char*)a.rec.payload, sizeof(a.rec.payload));
+  if (a.rec.kind == kvd::vmm::kPosixFd) {
+    for (uint64_t v : {(uint64_t)a.rec.fd, (uint64_t)pid, nonce, a.base, a.size})
+      k.append((const char*)&v, sizeof(v));
+  }
+  return k;
+}
+
+kvd_status map_open(const BlobAlloc& a, int64_t pid, uint64_t nonce, int device, void** out,
+                    std::string* key_out) {
   std::lock_guard<std::mutex> lk(g_map_mu);
-  auto key = std::make_pair(std::string((const char*)&h, sizeof(h)), device);
+  auto key = std::make_pair(map_key(a, pid, nonce), device);
+  *key_out = key.first;
   auto it = g_mappings.find(key);
   if (it != g_mappings.end()) {
     ++it->second.refs;
@@ -359,25 +387,46 @@ kvd_status ipc_open(const cudaIpcMemHandle_t& h, int device, void** out) {
     return KVD_OK;
   }
   void* p = nullptr;
-  cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    return fail(KVD_EHANDLE, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+  if (a.rec.kind == kvd::vmm::kLegacyIpc) {
+    cudaIpcMemHandle_t h;
+    memcpy(&h, a.rec.payload, sizeof(h));
+    cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(KVD_EHANDLE, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+    }
+  } else {
+    std::string err;
+    int s = kvd::vmm::import_map(a.rec, pid, a.size, device, &p, &err);
+    if (s != KVD_OK) return fail((kvd_status)s, "%s", err.c_str());
   }
-  g_mappings[key] = Mapping{p, 1};
+  g_mappings[key] = Mapping{p, 1, a.rec.kind, a.size};
   *out = p;
   return KVD_OK;
 }
 
-void ipc_close(const cudaIpcMemHandle_t& h, int device) {
+void map_close(const std::string& k, int device) {
   std::lock_guard<std::mutex> lk(g_map_mu);
-  auto key = std::make_pair(std::string((const char*)&h, sizeof(h)), device);
-  auto it = g_mappings.find(key);
+  auto it = g_mappings.find(std::make_pair(k, device));
   if (it == g_mappings.end()) return;
   if (--it->second.refs == 0) {
-    cudaIpcCloseMemHandle(it->second.ptr);
+    if (it->second.kind == kvd::vmm::kLegacyIpc) cudaIpcCloseMemHandle(it->second.ptr);
+    else kvd::vmm::unmap(it->second.ptr, it->second.size);
     g_mappings.erase(it);
   }
+}
+
+// The allocation holding addr: a kvd_mem_alloc range, else the driver's view.
+bool alloc_range(uint64_t addr, uint64_t* base, uint64_t* size) {
+  if (kvd::vmm::find(addr, base, size)) return true;
+  auto range = get_address_range_fn();
+  if (!range) return false;
+  unsigned long long b = 0;
+  size_t n = 0;
+  if (range(&b, &n, (unsigned long long)addr) != 0) return false;
+  *base = b;
+  *size = n;
+  return true;
 }
 
 }  // namespace
@@ -410,7 +459,7 @@ struct kvd_peer_s {
   Geom remote;
   int remote_device = -1;
   bool same_process = false;
-  std::vector<cudaIpcMemHandle_t> opened;  // handles we opened (to close)
+  std::vector<std::string> opened;         // mapping keys we opened (to close)
   unsigned long long* mbox = nullptr;       // the exporter's release mailbox, mapped here
   unsigned long long* d_src_bases = nullptr;
   std::vector<uint64_t> src_bases;         // host copy of the mapped remote layer bases
@@ -628,11 +677,10 @@ kvd_status kvd_register_cache(int device, const kvd_layout* layout, void* const*
   DeviceGuard dg(device);
   if (!dg.ok) return fail(KVD_ECUDA, "cannot select device %d", device);
   // every layer's extent must lie inside one allocation
-  if (auto range = get_address_range_fn()) {
+  if (get_address_range_fn()) {
     for (uint32_t l = 0; l < g.layout.num_layers; ++l) {
-      unsigned long long abase = 0;
-      size_t asize = 0;
-      if (range(&abase, &asize, (unsigned long long)bases[l]) != 0)
+      uint64_t abase = 0, asize = 0;
+      if (!alloc_range(bases[l], &abase, &asize))
         return fail(KVD_EINVAL, "layer %u base is not device memory", l);
       if (bases[l] + g.g.layer_bytes > abase + asize)
         return fail(KVD_ELAYOUT, "layer %u extent (%llu B) overruns its allocation", l,
@@ -663,14 +711,43 @@ kvd_status kvd_unregister_cache(kvd_cache c) {
 }
 
 // ===========================================================================
+// ABI: §8 f3 groundwork -- exportable (VMM) cache memory
+// ===========================================================================
+kvd_status kvd_mem_alloc(int device, uint64_t bytes, int kind, void** ptr, uint64_t* size,
+                         int* kind_out) {
+  if (!ptr || !bytes) return fail(KVD_EINVAL, "null pointer or zero size");
+  if (kind != KVD_MEM_AUTO && kind != KVD_MEM_POSIX_FD && kind != KVD_MEM_FABRIC)
+    return fail(KVD_EINVAL, "unknown memory kind %d", kind);
+  *ptr = nullptr;
+  DeviceGuard dg(device);
+  if (device < 0 || !dg.ok) return fail(KVD_ECUDA, "cannot select device %d", device);
+  uint64_t sz = 0;
+  uint32_t k = 0;
+  std::string err;
+  int s = kvd::vmm::alloc(device, bytes, (uint32_t)kind, ptr, &sz, &k, &err);
+  if (s != KVD_OK) return fail((kvd_status)s, "%s", err.c_str());
+  if (size) *size = sz;
+  if (kind_out) *kind_out = (int)k;
+  return KVD_OK;
+}
+
+kvd_status kvd_mem_free(void* ptr) {
+  if (!ptr) return fail(KVD_EINVAL, "null pointer");
+  std::string err;
+  int s = kvd::vmm::free(ptr, &err);
+  if (s != KVD_OK) return fail((kvd_status)s, "%s", err.c_str());
+  return KVD_OK;
+}
+
+// ===========================================================================
 // ABI: a2 export / open
 // ===========================================================================
 kvd_status kvd_export_handle(kvd_cache c, void* blob, size_t* blob_len) {
   if (!c || !blob_len) return fail(KVD_EINVAL, "null argument");
   DeviceGuard dg(c->device);
   if (!dg.ok) return fail(KVD_ECUDA, "cannot select device %d", c->device);
-  auto range = get_address_range_fn();
-  if (!range) return fail(KVD_ECUDA, "cuMemGetAddressRange entry point unavailable");
+  if (!get_address_range_fn())
+    return fail(KVD_ECUDA, "cuMemGetAddressRange entry point unavailable");
   Blob B;
   B.device = c->device;
   B.pid = (int64_t)getpid();
@@ -678,19 +755,28 @@ kvd_status kvd_export_handle(kvd_cache c, void* blob, size_t* blob_len) {
   B.layout = c->geom.layout;
   std::map<uint64_t, uint32_t> index;
   for (uint32_t l = 0; l < c->bases.size(); ++l) {
-    unsigned long long abase = 0;
-    size_t asize = 0;
-    if (range(&abase, &asize, (unsigned long long)c->bases[l]) != 0)
+    uint64_t abase = 0, asize = 0;
+    if (!alloc_range(c->bases[l], &abase, &asize))
       return fail(KVD_EHANDLE, "layer %u: cuMemGetAddressRange failed", l);
     auto it = index.find(abase);
     if (it == index.end()) {
       BlobAlloc a{};
-      cudaError_t e = cudaIpcGetMemHandle(&a.handle, (void*)(uintptr_t)abase);
-      if (e != cudaSuccess) {
-        cudaGetLastError();
-        return fail(KVD_EHANDLE,
-                    "cudaIpcGetMemHandle(layer %u): %s -- memory must come from cudaMalloc "
-                    "(not VMM / expandable segments)", l, cudaGetErrorString(e));
+      std::string err;
+      uint64_t vsize = 0;
+      const int v = kvd::vmm::lookup_export(abase, &vsize, &a.rec, &err);
+      if (v < 0) return fail((kvd_status)v, "layer %u: %s", l, err.c_str());
+      if (v == 0) {
+        cudaIpcMemHandle_t h;
+        cudaError_t e = cudaIpcGetMemHandle(&h, (void*)(uintptr_t)abase);
+        if (e != cudaSuccess) {
+          cudaGetLastError();
+          return fail(KVD_EHANDLE,
+                      "cudaIpcGetMemHandle(layer %u): %s -- memory must come from cudaMalloc "
+                      "or kvd_mem_alloc (not torch expandable segments)", l,
+                      cudaGetErrorString(e));
+        }
+        a.rec.kind = kvd::vmm::kLegacyIpc;
+        memcpy(a.rec.payload, &h, sizeof(h));
       }
       a.base = abase;
       a.size = asize;
@@ -708,11 +794,14 @@ kvd_status kvd_export_handle(kvd_cache c, void* blob, size_t* blob_len) {
       KVD_CUDA(cudaDeviceSynchronize());
       c->mbox_head = 0;
     }
-    cudaError_t e = cudaIpcGetMemHandle(&B.mbox.handle, c->mbox_dev);
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, c->mbox_dev);
     if (e != cudaSuccess) {
       cudaGetLastError();
       return fail(KVD_EHANDLE, "cudaIpcGetMemHandle(mailbox): %s", cudaGetErrorString(e));
     }
+    B.mbox.rec.kind = kvd::vmm::kLegacyIpc;
+    memcpy(B.mbox.rec.payload, &h, sizeof(h));
     B.has_mbox = true;
     B.mbox.base = (uint64_t)(uintptr_t)c->mbox_dev;
     B.mbox.size = kvd::kMailboxWords * sizeof(unsigned long long);
@@ -729,7 +818,7 @@ kvd_status kvd_export_handle(kvd_cache c, void* blob, size_t* blob_len) {
 static void peer_release(kvd_peer p) {
   if (!p) return;
   DeviceGuard dg(p->local ? p->local->device : 0);
-  for (auto& h : p->opened) ipc_close(h, p->local->device);
+  for (auto& k : p->opened) map_close(k, p->local->device);
   if (p->d_src_bases) cudaFree(p->d_src_bases);
   if (p->flags) cudaFreeHost(p->flags);
   if (p->counters) cudaFree(p->counters);
@@ -817,13 +906,21 @@ static kvd_status open_impl(kvd_cache local, const void* blob, size_t blob_len,
       cudaError_t e = cudaDeviceEnablePeerAccess(B.device, 0);
       if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
       else if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+      // VMM ranges ignore peer access: grant this device access to each
+      for (auto& a : B.allocs) {
+        if (a.rec.kind == kvd::vmm::kLegacyIpc) continue;
+        std::string err;
+        int g = kvd::vmm::grant_access(a.base, local->device, &err);
+        if (g != KVD_OK) return fail((kvd_status)g, "%s", err.c_str());
+      }
     }
   } else {
     for (size_t i = 0; i < B.allocs.size(); ++i) {
       void* ptr = nullptr;
-      s = ipc_open(B.allocs[i].handle, local->device, &ptr);
+      std::string key;
+      s = map_open(B.allocs[i], B.pid, B.nonce, local->device, &ptr, &key);
       if (s != KVD_OK) return s;
-      p->opened.push_back(B.allocs[i].handle);
+      p->opened.push_back(key);
       alloc_va[i] = (uint64_t)(uintptr_t)ptr;
     }
   }
@@ -834,9 +931,10 @@ static kvd_status open_impl(kvd_cache local, const void* blob, size_t blob_len,
       p->mbox = (unsigned long long*)(uintptr_t)B.mbox.base;
     } else {
       void* ptr = nullptr;
-      s = ipc_open(B.mbox.handle, local->device, &ptr);
+      std::string key;
+      s = map_open(B.mbox, B.pid, B.nonce, local->device, &ptr, &key);
       if (s != KVD_OK) return s;
-      p->opened.push_back(B.mbox.handle);
+      p->opened.push_back(key);
       p->mbox = (unsigned long long*)ptr;
     }
   }

@@ -20,12 +20,14 @@ LIB_PATH = os.environ.get("KVD_LIB_PATH") or os.path.join(_HERE, "libkvd.so")   
 OK, EINVAL, ERANGE, ELAYOUT, EHANDLE, ECUDA, ENOMEM, EBUSY, ESTATE = 0, -1, -2, -3, -4, -5, -6, -7, -8
 FP16, BF16, FP8, FP32 = 0, 1, 2, 3
 VARIANT_AUTO, VARIANT_LSU, VARIANT_LSU32, VARIANT_CE, VARIANT_TMA = 0, 1, 2, 3, 4
+MEM_AUTO, MEM_POSIX_FD, MEM_FABRIC = 0, 1, 8
 OPT_MAX_CTAS, OPT_TILE_BYTES, OPT_COALESCE, OPT_VARIANT, OPT_THREADS, OPT_STAGES = 0, 1, 2, 3, 4, 5
 OPT_AUDIT, OPT_TIMING = 6, 7
 
 EXPORTED = (
     "kvd_layout_geometry", "kvd_plan", "kvd_blob_info", "kvd_register_cache",
-    "kvd_unregister_cache", "kvd_export_handle", "kvd_open_peer", "kvd_open_peer_heads",
+    "kvd_unregister_cache", "kvd_mem_alloc", "kvd_mem_free", "kvd_export_handle", "kvd_open_peer",
+    "kvd_open_peer_heads",
     "kvd_close_peer",
     "kvd_peer_set", "kvd_pull", "kvd_push", "kvd_pull_batch", "kvd_poll_done", "kvd_wait_done",
     "kvd_last_pull_info", "kvd_peer_audit", "kvd_peer_kernel_time", "kvd_poll_released",
@@ -88,6 +90,9 @@ _SIGS = {
     "kvd_register_cache": [ctypes.c_int, ctypes.POINTER(kvd_layout), ctypes.POINTER(_p),
                            ctypes.POINTER(_p)],
     "kvd_unregister_cache": [_p],
+    "kvd_mem_alloc": [ctypes.c_int, _u64, ctypes.c_int, ctypes.POINTER(_p), ctypes.POINTER(_u64),
+                      ctypes.POINTER(ctypes.c_int)],
+    "kvd_mem_free": [_p],
     "kvd_export_handle": [_p, _p, ctypes.POINTER(ctypes.c_size_t)],
     "kvd_open_peer": [_p, _p, ctypes.c_size_t, ctypes.POINTER(_p)],
     "kvd_open_peer_heads": [_p, _p, ctypes.c_size_t, _u32, ctypes.POINTER(_p)],
@@ -195,6 +200,18 @@ def kvd_register_cache(device: int, layout: kvd_layout, layer_base_dev: Sequence
 
 def kvd_unregister_cache(cache: int) -> None:
     _check(_lib.kvd_unregister_cache(cache), "kvd_unregister_cache")
+
+
+def kvd_mem_alloc(device: int, nbytes: int, kind: int = MEM_AUTO):
+    """§8 f3 groundwork: exportable VMM memory.  Returns (ptr, size, kind)."""
+    ptr, size, k = _p(), _u64(0), ctypes.c_int(0)
+    _check(_lib.kvd_mem_alloc(int(device), int(nbytes), int(kind), ctypes.byref(ptr),
+                              ctypes.byref(size), ctypes.byref(k)), "kvd_mem_alloc")
+    return ptr.value, size.value, k.value
+
+
+def kvd_mem_free(ptr: int) -> None:
+    _check(_lib.kvd_mem_free(ptr), "kvd_mem_free")
 
 
 def kvd_export_handle(cache: int) -> bytes:

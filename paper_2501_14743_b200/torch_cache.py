@@ -5,6 +5,9 @@ one uint8 tensor per layer (vLLM keeps one tensor per layer) -- or one
 tensor sliced into layers -- sized by the library's own geometry
 (kvd_layout_geometry), and registers the layer bases with
 kvd_register_cache.  Every byte of a pull is moved by libkvd's kernel.
+With ``memory="vmm"`` the cache lives in one kvd_mem_alloc allocation (CUDA
+VMM, exported as a POSIX fd or fabric handle -- §8 f3 groundwork) that torch
+only views through ``__cuda_array_interface__``.
 """
 from __future__ import annotations
 
@@ -15,10 +18,19 @@ import torch
 from . import kvd
 
 
+class _DeviceBytes:
+    """A raw device range as a CUDA-array-interface object (no ownership)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1",
+                                         "data": (ptr, False), "version": 3, "strides": None}
+
+
 class PagedCache:
     def __init__(self, num_layers: int, num_kv_heads: int, head_dim: int, block_size: int,
                  num_blocks: int, dtype: int = kvd.FP16, stride: Sequence[int] = (0,) * 5,
-                 device: int = 0, single_allocation: bool = False, pad_bytes: int = 0):
+                 device: int = 0, single_allocation: bool = False, pad_bytes: int = 0,
+                 memory: str = "torch", mem_kind: int = kvd.MEM_AUTO):
         self.layout = kvd.make_layout(num_layers, num_kv_heads, head_dim, block_size, num_blocks,
                                       dtype, stride)
         self.geom = kvd.kvd_layout_geometry(self.layout)
@@ -27,7 +39,21 @@ class PagedCache:
         # round each layer to 512 B so every base stays 32 B aligned
         self.layer_pitch = (self.layer_bytes + pad_bytes + 511) // 512 * 512
         dev = torch.device("cuda", self.device)
-        if single_allocation:
+        self._vmm_ptr = None
+        self.mem_kind = None
+        if memory == "vmm":
+            ptr, _, self.mem_kind = kvd.kvd_mem_alloc(self.device, self.layer_pitch * num_layers,
+                                                      mem_kind)
+            self._vmm_ptr = ptr
+            with torch.cuda.device(self.device):
+                self._storage = torch.as_tensor(
+                    _DeviceBytes(ptr, self.layer_pitch * num_layers), device=dev)
+            self.layers = [
+                self._storage[l * self.layer_pitch:l * self.layer_pitch + self.layer_bytes]
+                for l in range(num_layers)]
+        elif memory != "torch":
+            raise ValueError(f"memory must be 'torch' or 'vmm', not {memory!r}")
+        elif single_allocation:
             self._storage = torch.empty(self.layer_pitch * num_layers, dtype=torch.uint8,
                                         device=dev)
             self.layers: List[torch.Tensor] = [
@@ -64,9 +90,15 @@ class PagedCache:
         return Peer(self, kvd.kvd_open_peer_heads(self.handle, blob, head_offset))
 
     def close(self) -> None:
+        """Unregister; a ``memory="vmm"`` cache also frees its memory (the
+        layer tensors are invalid afterwards)."""
         if self.handle:
             kvd.kvd_unregister_cache(self.handle)
             self.handle = None
+        if self._vmm_ptr:
+            self.layers, self._storage = [], None
+            kvd.kvd_mem_free(self._vmm_ptr)
+            self._vmm_ptr = None
 
     def __del__(self):
         try:

@@ -18,10 +18,11 @@ from paper_2501_14743_b200 import kvd
 from paper_2501_14743_b200.torch_cache import PagedCache, Peer
 
 
-def cache_for(geom: kvdgen.CacheGeom, device: int, single_allocation=False) -> PagedCache:
+def cache_for(geom: kvdgen.CacheGeom, device: int, single_allocation=False,
+              memory="torch", mem_kind=kvd.MEM_AUTO) -> PagedCache:
     return PagedCache(geom.num_layers, geom.num_kv_heads, geom.head_dim, geom.block_size,
                       geom.num_blocks, geom.dtype, geom.stride, device,
-                      single_allocation=single_allocation)
+                      single_allocation=single_allocation, memory=memory, mem_kind=mem_kind)
 
 
 def oracle_layer_bytes(geom: kvdgen.CacheGeom) -> int:
@@ -66,9 +67,9 @@ class Pair:
 
 
 def make_pair(sg: kvdgen.CacheGeom, dg: kvdgen.CacheGeom, seed: int, src_dev=0, dst_dev=0,
-              single_allocation=False) -> Pair:
-    src = cache_for(sg, src_dev, single_allocation)
-    dst = cache_for(dg, dst_dev, single_allocation)
+              single_allocation=False, src_memory="torch", dst_memory="torch") -> Pair:
+    src = cache_for(sg, src_dev, single_allocation, src_memory)
+    dst = cache_for(dg, dst_dev, single_allocation, dst_memory)
     assert src.layer_bytes == oracle_layer_bytes(sg)
     assert dst.layer_bytes == oracle_layer_bytes(dg)
     src_host = [kvdgen.random_bytes(src.layer_bytes, seed * 7919 + l) for l in range(sg.num_layers)]

@@ -15,9 +15,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 MAGIC = 0x4244564B
 
 
-def make_blob(device, pid, layers=3, allocs=2, num_blocks=64):
-    """A blob in the wire format of kvd_export_handle (test-side encoder)."""
-    b = struct.pack("<IIII", MAGIC, 2, device, 0)
+def make_blob(device, pid, layers=3, allocs=2, num_blocks=64, kinds=None):
+    """A blob in the wire format of kvd_export_handle, v3 (test-side encoder).
+    kinds: per-allocation handle kind (0 legacy IPC, 1 POSIX fd, 8 fabric)."""
+    kinds = kinds or [0] * allocs
+    b = struct.pack("<IIII", MAGIC, 3, device, 0)
     b += struct.pack("<QQ", pid, 0xABCDEF)
     b += struct.pack("<IIIIII", layers, 2, 64, 16, num_blocks, 0)   # layers, heads, dim, bs, nb, fp16
     sub = 16 * 2 * 64
@@ -25,6 +27,7 @@ def make_blob(device, pid, layers=3, allocs=2, num_blocks=64):
     b += struct.pack("<II", allocs, layers)
     layer_bytes = 2 * num_blocks * sub * 2
     for a in range(allocs):
+        b += struct.pack("<II", kinds[a], 17 + a if kinds[a] == 1 else 0)
         b += bytes([a + 1]) * 64 + struct.pack("<QQ", 0x7F0000000000 + a * (1 << 32),
                                                layers * layer_bytes)
     for l in range(layers):
@@ -123,3 +126,19 @@ def test_synthesised_blob_round_trip_and_corruption():
     bad[off:off + 4] = struct.pack("<I", 7)
     with pytest.raises(kvd.KvdError):
         kvd.kvd_blob_info(bytes(bad))
+
+
+def test_blob_handle_kinds():
+    """Blob v3 records a handle kind per allocation (legacy IPC, POSIX fd,
+    fabric -- §8 f3 groundwork); unknown kinds and older versions are refused."""
+    from paper_2501_14743_b200 import kvd
+    for kinds in ([0, 0], [1, 1], [8, 0], [1, 8]):
+        _, _, _, na = kvd.kvd_blob_info(make_blob(0, 1, kinds=kinds))
+        assert na == 2
+    with pytest.raises(kvd.KvdError) as ei:
+        kvd.kvd_blob_info(make_blob(0, 1, kinds=[2, 0]))
+    assert ei.value.status == kvd.EHANDLE
+    old = bytearray(make_blob(0, 1))
+    old[4:8] = struct.pack("<I", 2)
+    with pytest.raises(kvd.KvdError):
+        kvd.kvd_blob_info(bytes(old))
