@@ -1095,7 +1095,7 @@ static Policy choose_policy(const kvd_peer_s* p, uint64_t req_bytes, uint64_t av
 // Threads per CTA, TMA ring depth and grid size of a tiled launch.
 static kvd_status launch_shape(const kvd_peer_s* p, Policy& P, kvd::PullArgs& a,
                                uint64_t bytes, uint32_t* threads_out, uint32_t* ctas_out) {
-  const uint32_t threads =
+  uint32_t threads =
       p->threads_set ? p->threads
                      : (P.variant == KVD_VARIANT_TMA ? (P.tma_defaults ? 32u * P.pipes : 96u)
                                                      : (P.small ? 32u : 512u));
@@ -1107,7 +1107,7 @@ static kvd_status launch_shape(const kvd_peer_s* p, Policy& P, kvd::PullArgs& a,
           2, (225u * 1024u) / ((threads / 32) * (uint64_t)a.tile_bytes));
       smem = (uint64_t)(threads / 32) * P.stages * a.tile_bytes;
     }
-    if (smem > 225u * 1024u)   // 227 KiB per CTA minus the 2 KiB mbarrier array
+    if (smem > 225u * 1024u)   // 227 KiB per CTA minus the static mbarriers / flags
       return fail(KVD_EINVAL, "TMA ring needs %llu B of shared memory (pipes %u x stages %u x "
                   "tile %u); max 225 KiB", (unsigned long long)smem, threads / 32, P.stages,
                   a.tile_bytes);
@@ -1133,6 +1133,13 @@ static kvd_status launch_shape(const kvd_peer_s* p, Policy& P, kvd::PullArgs& a,
   }
   // small requests: one tile per warp, so every tile is in flight at once
   a.tiles_per_warp = P.small ? 1u : kvd::lsu_tiles_per_warp();
+  if (P.autov && P.variant != KVD_VARIANT_TMA && !P.small && !p->threads_set) {
+    // medium requests (a few MiB to tens of MiB): spread over every SM before
+    // batching tiles per warp -- at least two CTAs per SM, narrower CTAs first
+    const uint64_t want = 2ull * (uint64_t)p->sm_count;
+    if (grid_for(a.total_tiles, threads, max_ctas, a.tiles_per_warp) < want) a.tiles_per_warp = 1;
+    while (threads > 32 && grid_for(a.total_tiles, threads, max_ctas, 1) < want) threads >>= 1;
+  }
   *threads_out = threads;
   *ctas_out = grid_for(a.total_tiles, threads, max_ctas,
                        P.variant == KVD_VARIANT_TMA ? 1u : a.tiles_per_warp);

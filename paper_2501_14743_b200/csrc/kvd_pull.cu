@@ -87,8 +87,14 @@ __device__ __forceinline__ void st_local(V32* p, const V32& v) {
                   "r"(v.v[4]), "r"(v.v[5]), "r"(v.v[6]), "r"(v.v[7]) : "memory");
 }
 
+// A system-scope release costs ~1.5 us on B200 (tools/native/fence_probe.cu:
+// ~3000 SM cycles, the same as fence.sc.sys; a gpu-scope fence ~200), so the
+// completion path issues as few of them as the ordering needs.
 __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() {
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
 
 // One warp copies `bytes` (multiple of sizeof(V)) from src to dst.  All U
@@ -248,22 +254,25 @@ __device__ __forceinline__ bool tile_in_bounds(const PullArgs& a, const Tile& T,
 // Complete() to the prefill side ("The completion transaction sends
 // the request ID to the prefill worker"; it then releases the
 // blocks): claim a slot of the exporter's mailbox with a system-scope atomic
-// over NVLink, write the id, then release the slot's sequence word.  Called
-// after every byte of the request has landed, i.e. after its last remote read.
+// over NVLink, write the id, then release the slot's sequence word (the
+// release orders the id store before it).  Called after every byte of the
+// request has landed, i.e. after its last remote read.
 __device__ __forceinline__ void notify_release(const PullArgs& a, unsigned long long request_id) {
   if (a.mbox == nullptr) return;
   const unsigned long long s = atomicAdd_system(a.mbox, 1ull);
   unsigned long long* e = a.mbox + 8 + 2 * (s % kReleaseRing);
   *(volatile unsigned long long*)(e + 1) = request_id;
-  __threadfence_system();
   st_release_sys(e, s + 1);
 }
 
 // --- batched drain (f1): per-request completion inside one launch ----------
+// The caller's atomic observed every credit of request q; the acquire fence
+// makes their (fenced) stores happen-before this thread's system-scope
+// release of the slot word (causality is transitive across the two scopes).
 __device__ __forceinline__ void publish(const PullArgs& a, unsigned int q) {
   const uint4 R = a.reqs[q];
   a.bytectr[R.y] = 0ull;                 // slot idle again
-  __threadfence_system();
+  fence_acq_rel_gpu();
   st_release_sys(&a.flags[R.y], a.tokens[q]);
   notify_release(a, a.req_ids[q]);
 }
@@ -343,22 +352,35 @@ __device__ __forceinline__ void publish_empty(const PullArgs& a) {
 
 // Completion (row a6): every thread orders its stores (gpu scope for the
 // pull's local stores, system scope when push stored into a peer GPU), the
-// CTA arrives once; the last CTA resets the slot counter and publishes the
-// token with a system-scope release, so a host acquire load of the word
-// implies every byte landed.
+// CTA arrives once; the last CTA acquires (gpu scope: every arrival is on
+// this GPU), resets the slot counter and publishes the token with ONE
+// system-scope release, so a host acquire load of the word implies every
+// byte landed.  The prefill-side notification follows; with a second warp
+// it runs in parallel with the host release instead of after it.
 __device__ __forceinline__ void complete(const PullArgs& a) {
   if (a.counter == nullptr) return;   // baseline gather/scatter: stream order only
   if (a.remote_stores) __threadfence_system(); else __threadfence();
+  __shared__ unsigned int s_last;
   __syncthreads();
   if (threadIdx.x == 0) {
     const unsigned int prev = atomicAdd(a.counter, 1u);
-    if (prev == gridDim.x - 1) {
+    s_last = prev == gridDim.x - 1;
+    if (s_last) {
       *a.counter = 0u;
-      __threadfence_system();
+      fence_acq_rel_gpu();
+    }
+  }
+  if (blockDim.x < 64) {
+    if (threadIdx.x == 0 && s_last) {
       st_release_sys(a.flag, a.token);
       notify_release(a, a.request_id);
     }
+    return;
   }
+  __syncthreads();                    // warp 1 synchronises with thread 0's acquire
+  if (!s_last) return;
+  if (threadIdx.x == 0) st_release_sys(a.flag, a.token);
+  else if (threadIdx.x == 32) notify_release(a, a.request_id);
 }
 
 // Stage the run table in shared memory when the launcher reserved room for
@@ -472,7 +494,7 @@ template <int MAXR>
 __global__ void __launch_bounds__(256)
 pull_kernel_tma(const __grid_constant__ PullParams<MAXR> P, unsigned int stages) {
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ uint64_t bars[32 * kMaxStages];
+  __shared__ uint64_t bars[(256 / 32) * kMaxStages];   // <= 8 pipes (launch bound)
   const PullArgs& a = P.a;
   const unsigned int warp = threadIdx.x >> 5;
   const unsigned int pipes_per_cta = blockDim.x >> 5;
@@ -541,7 +563,7 @@ pull_kernel_tma(const __grid_constant__ PullParams<MAXR> P, unsigned int stages)
 
 __global__ void flag_kernel(unsigned long long* flag, unsigned long long token,
                             unsigned long long* mbox, unsigned long long request_id) {
-  __threadfence_system();
+  // no data: earlier stream work is ordered by the stream itself
   st_release_sys(flag, token);
   PullArgs a{};
   a.mbox = mbox;

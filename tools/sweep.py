@@ -93,10 +93,11 @@ def main():
 
     if a.profile_once:
         s, d = tables(g, a.tables.split(",")[0], n)
-        peer.set(kvd.OPT_VARIANT, VAR[a.variants.split(",")[0]])
-        peer.set(kvd.OPT_TILE_BYTES, int(a.tiles.split(",")[0]))
-        peer.set(kvd.OPT_THREADS, int(a.threads.split(",")[0]))
-        peer.set(kvd.OPT_MAX_CTAS, int(a.ctas.split(",")[0]))
+        if a.variants != "auto":     # "auto": the library's own launch policy (bench default)
+            peer.set(kvd.OPT_VARIANT, VAR[a.variants.split(",")[0]])
+            peer.set(kvd.OPT_TILE_BYTES, int(a.tiles.split(",")[0]))
+            peer.set(kvd.OPT_THREADS, int(a.threads.split(",")[0]))
+            peer.set(kvd.OPT_MAX_CTAS, int(a.ctas.split(",")[0]))
         pull(s, d)
         torch.cuda.synchronize()
         pull(s, d)
