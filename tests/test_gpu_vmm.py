@@ -141,3 +141,27 @@ def test_vmm_pull_across_processes(devs):
     ok, kind = result.get(timeout=5)
     assert ok is True and kind in (kvd.MEM_POSIX_FD, kvd.MEM_FABRIC)
     assert released.get(timeout=5) == [8000, 8001, 8002]
+
+
+def test_vmm_push_and_batch():
+    """f2 push into an imported VMM decode cache, and an f1 batched drain from
+    a VMM prefill cache: same oracle bytes as with cudaMalloc memory."""
+    pair = make_pair(G, G, seed=92, src_memory="vmm", dst_memory="vmm")
+    try:
+        (s1, d1), (s2, d2), (s3, d3) = kvdgen.disjoint_fragmented_tables([50, 70, 30], 256, 256,
+                                                                         seed=12)
+        rev = pair.src.open_peer(pair.dst.export())   # prefill side imports the decode cache
+        rid = next_request_id()
+        rev.push(rid, s1, d1)
+        rev.wait(rid)
+        rev.close()
+        exp = pair.expected(s1, d1)
+        ids = [next_request_id(), next_request_id()]
+        pair.peer.pull_batch(ids, [(s2, d2), (s3, d3)])
+        for r in ids:
+            pair.peer.wait(r)
+        exp = pair.expected(s3, d3, pair.expected(s2, d2, exp))
+        assert_layers_equal(pair.download_dst(), exp)
+        assert sorted(pair.src.poll_released()) == sorted(ids)
+    finally:
+        pair.close()
