@@ -260,6 +260,9 @@ KVD_API kvd_status kvd_open_peer(kvd_cache local_dst, const void* blob, size_t b
 KVD_API kvd_status kvd_open_peer_heads(kvd_cache local_dst, const void* blob, size_t blob_len,
                                        uint32_t head_offset, kvd_peer* out);
 
+/* Close a peer: synchronises the local device (transfers still in flight
+ * finish first), unmaps the imported allocations and frees the completion
+ * slots.  Request ids not yet polled are forgotten. */
 KVD_API kvd_status kvd_close_peer(kvd_peer peer);
 
 /* Tune a peer (see kvd_option).  KVD_EINVAL on an unknown option/value. */

@@ -818,6 +818,9 @@ kvd_status kvd_export_handle(kvd_cache c, void* blob, size_t* blob_len) {
 static void peer_release(kvd_peer p) {
   if (!p) return;
   DeviceGuard dg(p->local ? p->local->device : 0);
+  // pulls / pushes still in flight read or write through the mappings: let
+  // them finish before anything is unmapped or freed (close is not hot)
+  if (p->local) cudaDeviceSynchronize();
   for (auto& k : p->opened) map_close(k, p->local->device);
   if (p->d_src_bases) cudaFree(p->d_src_bases);
   if (p->flags) cudaFreeHost(p->flags);

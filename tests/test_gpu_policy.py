@@ -1,0 +1,68 @@
+"""The auto launch policy: which mover and grid a request gets,
+checked through kvd_last_pull_info, each case also bit-exact against the
+oracle.  Small requests (<= 2 MiB) -> one-warp CTAs and 2 KiB tiles; medium
+loopback requests -> at least two CTAs per SM; over NVLink -> the TMA ring
+with >= 48 CTAs."""
+import pytest
+import torch
+
+import kvdgen
+from gpu_helpers import assert_layers_equal, make_pair, pull_and_wait
+
+pytestmark = pytest.mark.gpu
+
+G7B = kvdgen.C2.with_blocks(48)      # Llama-2-7B geometry, 8 MiB per block, small pools
+
+
+def _sms(dev=0):
+    return torch.cuda.get_device_properties(dev).multi_processor_count
+
+
+def test_small_request_policy():
+    g = kvdgen.C1
+    pair = make_pair(g, g, seed=101)
+    try:
+        s, d = kvdgen.fragmented_table(16, g.num_blocks, g.num_blocks, seed=3)
+        info = pull_and_wait(pair, s, d)
+        assert info["threads"] == 32 and info["variant"] == 2   # LSU32, one warp per CTA
+        assert info["tiles"] == info["ctas"]                     # one 2 KiB tile per warp
+        assert_layers_equal(pair.download_dst(), pair.expected(s, d))
+    finally:
+        pair.close()
+
+
+@pytest.mark.parametrize("blocks", [1, 2, 4, 16])
+def test_medium_loopback_request_spreads_over_the_gpu(blocks):
+    pair = make_pair(G7B, G7B, seed=102)
+    try:
+        s, d = kvdgen.fragmented_table(blocks, G7B.num_blocks, G7B.num_blocks, seed=blocks)
+        info = pull_and_wait(pair, s, d)
+        assert info["variant"] == 2
+        assert info["ctas"] >= min(2 * _sms(), info["tiles"]), info
+        assert_layers_equal(pair.download_dst(), pair.expected(s, d))
+    finally:
+        pair.close()
+
+
+def test_large_loopback_request_uses_full_chunks():
+    pair = make_pair(G7B, G7B, seed=103)
+    try:
+        s, d = kvdgen.fragmented_table(40, G7B.num_blocks, G7B.num_blocks, seed=4)
+        info = pull_and_wait(pair, s, d)
+        assert info["variant"] == 2 and info["threads"] == 512
+        assert_layers_equal(pair.download_dst(), pair.expected(s, d))
+    finally:
+        pair.close()
+
+
+def test_over_nvlink_uses_tma_ring():
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs")
+    pair = make_pair(G7B, G7B, seed=104, src_dev=0, dst_dev=1)
+    try:
+        s, d = kvdgen.fragmented_table(32, G7B.num_blocks, G7B.num_blocks, seed=5)
+        info = pull_and_wait(pair, s, d)
+        assert info["variant"] == 4 and info["ctas"] >= 48
+        assert_layers_equal(pair.download_dst(), pair.expected(s, d))
+    finally:
+        pair.close()
