@@ -447,7 +447,10 @@ struct kvd_cache_s {
   // release mailbox (exporter side): importers post completed request ids
   unsigned long long* mbox_dev = nullptr;
   uint64_t mbox_head = 0;                 // next sequence to consume
-  std::vector<unsigned long long> mbox_host;
+  // the mailbox is read on a private non-blocking stream into pinned memory,
+  // so polling never waits behind the exporter's own (prefill) work
+  cudaStream_t mbox_stream = nullptr;
+  unsigned long long* mbox_pinned = nullptr;
 };
 
 namespace {
@@ -705,6 +708,8 @@ kvd_status kvd_unregister_cache(kvd_cache c) {
     DeviceGuard dg(c->device);
     if (c->d_bases) cudaFree(c->d_bases);
     if (c->mbox_dev) cudaFree(c->mbox_dev);
+    if (c->mbox_stream) cudaStreamDestroy(c->mbox_stream);
+    if (c->mbox_pinned) cudaFreeHost(c->mbox_pinned);
   }
   delete c;
   return KVD_OK;
@@ -794,6 +799,10 @@ kvd_status kvd_export_handle(kvd_cache c, void* blob, size_t* blob_len) {
       KVD_CUDA(cudaDeviceSynchronize());
       c->mbox_head = 0;
     }
+    if (!c->mbox_stream)
+      KVD_CUDA(cudaStreamCreateWithFlags(&c->mbox_stream, cudaStreamNonBlocking));
+    if (!c->mbox_pinned)
+      KVD_CUDA(cudaMallocHost(&c->mbox_pinned, kvd::kMailboxWords * sizeof(unsigned long long)));
     cudaIpcMemHandle_t h;
     cudaError_t e = cudaIpcGetMemHandle(&h, c->mbox_dev);
     if (e != cudaSuccess) {
@@ -1513,10 +1522,13 @@ kvd_status kvd_poll_released(kvd_cache c, uint64_t* request_ids, uint32_t cap, u
   if (!c->mbox_dev) return KVD_OK;               // never exported: nobody can complete
   DeviceGuard dg(c->device);
   if (!dg.ok) return fail(KVD_ECUDA, "cannot select device %d", c->device);
-  c->mbox_host.resize(kvd::kMailboxWords);
-  KVD_CUDA(cudaMemcpy(c->mbox_host.data(), c->mbox_dev,
-                      kvd::kMailboxWords * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
-  const unsigned long long* ring = c->mbox_host.data() + 8;
+  // a plain cudaMemcpy would run on the legacy default stream and wait for
+  // whatever prefill work the exporter has queued there
+  KVD_CUDA(cudaMemcpyAsync(c->mbox_pinned, c->mbox_dev,
+                           kvd::kMailboxWords * sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, c->mbox_stream));
+  KVD_CUDA(cudaStreamSynchronize(c->mbox_stream));
+  const unsigned long long* ring = c->mbox_pinned + 8;
   uint32_t k = 0;
   while (k < cap) {
     const uint64_t slot = c->mbox_head % kvd::kReleaseRing;

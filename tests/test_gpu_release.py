@@ -103,3 +103,24 @@ def test_release_mailbox_two_gpus():
         assert sorted(got) == sorted(ids)
     finally:
         pair.close()
+
+
+def test_poll_released_does_not_wait_for_exporter_work():
+    """The exporter polls while its own GPU is busy (prefill kernels queued on
+    the default stream): the poll must not serialise behind that work."""
+    import time
+    pair = make_pair(G, G, seed=64)
+    try:
+        s, d = kvdgen.random_table(20, 256, 256, seed=5)
+        rid = next_request_id()
+        pair.peer.pull(rid, s, d)
+        pair.peer.wait(rid)
+        torch.cuda._sleep(1_500_000_000)          # ~0.75 s of "prefill" on the default stream
+        t0 = time.perf_counter()
+        got = pair.src.poll_released()
+        dt = time.perf_counter() - t0
+        torch.cuda.synchronize()
+        assert got == [rid]
+        assert dt < 0.3, f"poll_released waited {dt:.3f} s behind the default stream"
+    finally:
+        pair.close()
