@@ -256,13 +256,27 @@ __device__ __forceinline__ bool tile_in_bounds(const PullArgs& a, const Tile& T,
 // blocks): claim a slot of the exporter's mailbox with a system-scope atomic
 // over NVLink, write the id, then release the slot's sequence word (the
 // release orders the id store before it).  Called after every byte of the
-// request has landed, i.e. after its last remote read.
-__device__ __forceinline__ void notify_release(const PullArgs& a, unsigned long long request_id) {
+// request has landed, i.e. after its last remote read.  Split in two so the
+// claim's NVLink round trip (~1.5 us) overlaps the host-flag release that
+// sits between them (fence_probe: 4.5 -> 3.1 us for the whole sequence).
+__device__ __forceinline__ unsigned long long mbox_claim(const PullArgs& a) {
+  return a.mbox ? atomicAdd_system(a.mbox, 1ull) : 0ull;
+}
+__device__ __forceinline__ void mbox_post(const PullArgs& a, unsigned long long s,
+                                          unsigned long long request_id) {
   if (a.mbox == nullptr) return;
-  const unsigned long long s = atomicAdd_system(a.mbox, 1ull);
   unsigned long long* e = a.mbox + 8 + 2 * (s % kReleaseRing);
   *(volatile unsigned long long*)(e + 1) = request_id;
   st_release_sys(e, s + 1);
+}
+// Publish a finished request: claim the mailbox slot, release the token into
+// the host-visible slot word, then post the id to the exporter.
+__device__ __forceinline__ void publish_token(const PullArgs& a, unsigned long long* flag,
+                                              unsigned long long token,
+                                              unsigned long long request_id) {
+  const unsigned long long s = mbox_claim(a);
+  st_release_sys(flag, token);
+  mbox_post(a, s, request_id);
 }
 
 // --- batched drain (f1): per-request completion inside one launch ----------
@@ -273,8 +287,7 @@ __device__ __forceinline__ void publish(const PullArgs& a, unsigned int q) {
   const uint4 R = a.reqs[q];
   a.bytectr[R.y] = 0ull;                 // slot idle again
   fence_acq_rel_gpu();
-  st_release_sys(&a.flags[R.y], a.tokens[q]);
-  notify_release(a, a.req_ids[q]);
+  publish_token(a, &a.flags[R.y], a.tokens[q], a.req_ids[q]);
 }
 
 // Credit `bytes` landed bytes to request q; the credit that reaches the
@@ -355,32 +368,19 @@ __device__ __forceinline__ void publish_empty(const PullArgs& a) {
 // CTA arrives once; the last CTA acquires (gpu scope: every arrival is on
 // this GPU), resets the slot counter and publishes the token with ONE
 // system-scope release, so a host acquire load of the word implies every
-// byte landed.  The prefill-side notification follows; with a second warp
-// it runs in parallel with the host release instead of after it.
+// byte landed; the prefill-side notification follows (publish_token).
 __device__ __forceinline__ void complete(const PullArgs& a) {
   if (a.counter == nullptr) return;   // baseline gather/scatter: stream order only
   if (a.remote_stores) __threadfence_system(); else __threadfence();
-  __shared__ unsigned int s_last;
   __syncthreads();
   if (threadIdx.x == 0) {
     const unsigned int prev = atomicAdd(a.counter, 1u);
-    s_last = prev == gridDim.x - 1;
-    if (s_last) {
+    if (prev == gridDim.x - 1) {
       *a.counter = 0u;
       fence_acq_rel_gpu();
+      publish_token(a, a.flag, a.token, a.request_id);
     }
   }
-  if (blockDim.x < 64) {
-    if (threadIdx.x == 0 && s_last) {
-      st_release_sys(a.flag, a.token);
-      notify_release(a, a.request_id);
-    }
-    return;
-  }
-  __syncthreads();                    // warp 1 synchronises with thread 0's acquire
-  if (!s_last) return;
-  if (threadIdx.x == 0) st_release_sys(a.flag, a.token);
-  else if (threadIdx.x == 32) notify_release(a, a.request_id);
 }
 
 // Stage the run table in shared memory when the launcher reserved room for
@@ -564,10 +564,9 @@ pull_kernel_tma(const __grid_constant__ PullParams<MAXR> P, unsigned int stages)
 __global__ void flag_kernel(unsigned long long* flag, unsigned long long token,
                             unsigned long long* mbox, unsigned long long request_id) {
   // no data: earlier stream work is ordered by the stream itself
-  st_release_sys(flag, token);
   PullArgs a{};
   a.mbox = mbox;
-  notify_release(a, request_id);
+  publish_token(a, flag, token, request_id);
 }
 
 // ---------------------------------------------------------------------------

@@ -22,14 +22,19 @@
 enum Op {
   kNothing, kFenceGpu, kFenceSys, kRelSysHost, kRelSysDev, kAtomSysDev, kAtomSysPeer,
   kAtomGpuDev, kStoreHostFenceSys, kRelGpuDev, kStoresThenFenceGpu, kStoresThenFenceSys,
-  kNumOps
+  kAtomPeerUsed, kAtomPeerThenRelHost, kRelHostThenAtomPeerRelPeer, kAtomPeerRelHostRelPeer,
+  kTwoRelSys, kNumOps
 };
 const char* kName[kNumOps] = {
     "nothing", "fence.gpu (threadfence)", "fence.sys (threadfence_system)",
     "st.release.sys -> pinned host", "st.release.sys -> local HBM",
     "atomicAdd_system -> local HBM", "atomicAdd_system -> peer HBM (NVLink)",
     "atomicAdd (gpu) -> local HBM", "volatile st host + fence.sys", "st.release.gpu -> local HBM",
-    "1 MiB CTA stores then fence.gpu", "1 MiB CTA stores then fence.sys"};
+    "1 MiB CTA stores then fence.gpu", "1 MiB CTA stores then fence.sys",
+    "atomicAdd_system -> peer, result used", "peer atomic issued, then st.release.sys host (overlap?)",
+    "completion now: rel.sys host; peer atomic; st id; rel.sys peer",
+    "completion reordered: peer atomic; rel.sys host; st id; rel.sys peer",
+    "two st.release.sys back to back (host, local)"};
 
 __device__ __forceinline__ void st_rel_sys(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
@@ -62,6 +67,34 @@ __global__ void probe(int op, unsigned long long* host, unsigned long long* dev,
       case kRelGpuDev: st_rel_gpu(dev + 24, r); break;
       case kStoresThenFenceGpu: __threadfence(); break;
       case kStoresThenFenceSys: __threadfence_system(); break;
+      case kAtomPeerUsed: {
+        unsigned long long v = atomicAdd_system(peer, 1ull);
+        *(volatile unsigned long long*)(dev + 32) = v;
+        break;
+      }
+      case kAtomPeerThenRelHost: {
+        unsigned long long v = atomicAdd_system(peer, 1ull);
+        st_rel_sys(host, r);
+        *(volatile unsigned long long*)(dev + 32) = v;
+        break;
+      }
+      case kRelHostThenAtomPeerRelPeer: {
+        st_rel_sys(host, r);
+        unsigned long long v = atomicAdd_system(peer, 1ull);
+        unsigned long long* e = peer + 8 + 2 * (v % 64);
+        *(volatile unsigned long long*)(e + 1) = r;
+        st_rel_sys(e, v + 1);
+        break;
+      }
+      case kAtomPeerRelHostRelPeer: {
+        unsigned long long v = atomicAdd_system(peer, 1ull);
+        st_rel_sys(host, r);
+        unsigned long long* e = peer + 8 + 2 * (v % 64);
+        *(volatile unsigned long long*)(e + 1) = r;
+        st_rel_sys(e, v + 1);
+        break;
+      }
+      case kTwoRelSys: st_rel_sys(host, r); st_rel_sys(dev + 40, r); break;
       default: break;
     }
     const long long t1 = clock64();
@@ -87,8 +120,8 @@ int main(int argc, char** argv) {
   CK(cudaMalloc(&scratch, 1 << 20));
   if (ndev > 1) {
     CK(cudaSetDevice(1));
-    CK(cudaMalloc(&peer, 4096));
-    CK(cudaMemset(peer, 0, 4096));
+    CK(cudaMalloc(&peer, 8192));
+    CK(cudaMemset(peer, 0, 8192));
     CK(cudaSetDevice(0));
     CK(cudaDeviceEnablePeerAccess(1, 0));
   }
@@ -98,7 +131,8 @@ int main(int argc, char** argv) {
   CK(cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0));
   printf("{\"sm_clock_mhz\": %.0f}\n", clk_khz / 1e3);
   for (int op = 0; op < kNumOps; ++op) {
-    if (op == kAtomSysPeer && !peer) continue;
+    if ((op == kAtomSysPeer || (op >= kAtomPeerUsed && op <= kAtomPeerRelHostRelPeer)) && !peer)
+      continue;
     probe<<<1, 256>>>(op, host_dev, dev, peer, scratch, out, 16);
     CK(cudaDeviceSynchronize());
     const long long best = out[0];
