@@ -1373,13 +1373,13 @@ kvd_status kvd_pull_batch(kvd_peer p, uint32_t num_requests, const uint64_t* req
   a.dst = kvd::SideAddr{p->local->d_bases, 0, 0, dg_.plane_stride_bytes, dg_.block_stride_bytes};
   const uint64_t per_entry = (uint64_t)NL * 2 * sg.span_bytes;
   Policy pol = choose_policy(p, (uint64_t)n * per_entry, avg_segment(pp, n, p->runs.size()));
-  if (pol.autov && pol.variant == KVD_VARIANT_TMA) {
-    // batches: the TMA ring must wait for each store's completion before
-    // crediting it, which costs ~30% of its throughput; the full-grid LSU
-    // mover credits after a warp fence and stays at the link ceiling
-    pol.variant = KVD_VARIANT_LSU32;
-    pol.tma_defaults = false;
-    pol.tile = p->tile_bytes;
+  if (pol.tma_defaults && pol.pipes == 1 && !p->stages_set && !p->threads_set) {
+    // batches: a pipe credits a tile only after its bulk store completed, so
+    // a deep single ring idles behind the write acks; two pipes x 3 stages
+    // of 32 KiB keep the link full (C3 batched over NVLink: 785 GB/s vs 774
+    // for 1 x 6 and 770 for the full-grid LSU mover, tools/batch_sweep.sh)
+    pol.pipes = 2;
+    pol.stages = 3;
   }
   if (p->row_bytes) head_slice_plan(p, sg, pp, pol, a);
   s = tile_runs(p->runs, pp, NL, pol.tile, p->runs4, a, /*run_major=*/true);
