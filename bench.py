@@ -452,9 +452,11 @@ def run_kvd(args, rank, world, local_rank):
         retire(0, lat_out)
 
     def barrier():
+        # a host-side (gloo) barrier: an NCCL barrier would leave a spinning
+        # NCCL kernel on the prefill GPU for the whole timed region
         torch.cuda.synchronize()
         if multi:
-            dist.barrier()
+            dist.barrier(group=gloo)
 
     for _ in range(args.warmup):
         if peer:

@@ -1373,11 +1373,22 @@ kvd_status kvd_pull_batch(kvd_peer p, uint32_t num_requests, const uint64_t* req
   a.dst = kvd::SideAddr{p->local->d_bases, 0, 0, dg_.plane_stride_bytes, dg_.block_stride_bytes};
   const uint64_t per_entry = (uint64_t)NL * 2 * sg.span_bytes;
   Policy pol = choose_policy(p, (uint64_t)n * per_entry, avg_segment(pp, n, p->runs.size()));
-  if (pol.tma_defaults && pol.pipes == 1 && !p->stages_set && !p->threads_set) {
+  if (pol.tma_defaults && !p->threads_set && !p->stages_set &&
+      (uint64_t)n * per_entry < (uint64_t)num_requests * (512ull << 20)) {
+    // batches of short requests (< 512 MiB each on average): every request
+    // completion is a system-scope release + NVLink atomic, and issued from
+    // a TMA pipe those stall the ring (C2 128-token requests: 686 GB/s vs
+    // 758 with the full-grid LSU mover, tools/small_requests.py --ipc)
+    pol.variant = KVD_VARIANT_LSU32;
+    pol.tma_defaults = false;
+    pol.tile = p->tile_bytes;
+    pol.pipes = 1;
+  } else if (pol.tma_defaults && pol.pipes == 1 && !p->stages_set && !p->threads_set) {
     // batches: a pipe credits a tile only after its bulk store completed, so
     // a deep single ring idles behind the write acks; two pipes x 3 stages
-    // of 32 KiB keep the link full (C3 batched over NVLink: 785 GB/s vs 774
-    // for 1 x 6 and 770 for the full-grid LSU mover, tools/batch_sweep.sh)
+    // of 32 KiB keep the link full (C3 batched over NVLink: 782-785 GB/s vs
+    // 774 for 1 x 6 and 770-776 for the full-grid LSU mover,
+    // tools/batch_sweep.sh, tools/mover_ab_bench.sh)
     pol.pipes = 2;
     pol.stages = 3;
   }

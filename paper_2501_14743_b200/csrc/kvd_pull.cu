@@ -287,6 +287,13 @@ __device__ __forceinline__ void publish(const PullArgs& a, unsigned int q) {
   const uint4 R = a.reqs[q];
   a.bytectr[R.y] = 0ull;                 // slot idle again
   fence_acq_rel_gpu();
+#if defined(KVD_EXPERIMENT_PUBLISH_GPU_SCOPE)   // A/B experiment only: unsound for the host
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" :: "l"(&a.flags[R.y]), "l"(a.tokens[q]) : "memory");
+  return;
+#elif defined(KVD_EXPERIMENT_PUBLISH_NO_MBOX)   // A/B experiment only: no prefill notification
+  st_release_sys(&a.flags[R.y], a.tokens[q]);
+  return;
+#endif
   publish_token(a, &a.flags[R.y], a.tokens[q], a.req_ids[q]);
 }
 
@@ -300,6 +307,9 @@ __device__ __forceinline__ void credit(const PullArgs& a, unsigned int q, unsign
 }
 
 __device__ __forceinline__ void fence_stores(const PullArgs& a) {
+#ifdef KVD_EXPERIMENT_NO_CREDIT_FENCE   // A/B experiment only: unsound ordering
+  return;
+#endif
   if (a.remote_stores) __threadfence_system(); else __threadfence();
 }
 
@@ -513,9 +523,19 @@ pull_kernel_tma(const __grid_constant__ PullParams<MAXR> P, unsigned int stages)
     for (unsigned int s = 0; s < S; ++s) mbar_init(&bar[s]);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 
-    // tile i of this pipe = pipe + i * npipes
-    const unsigned int count =
-        pipe < a.total_tiles ? (a.total_tiles - pipe + npipes - 1) / npipes : 0u;
+    // Tile i of this pipe: pipes sweep the tile space in groups of K
+    // consecutive tiles, group g going to pipe g % npipes.  Single requests
+    // use K = 1 (plain grid stride).  Batches use K = 16: a pipe's tiles then
+    // mostly belong to one request, so a credit (fence + atomic round trip
+    // in the issuing lane) is paid per group, not per tile, while the sweep
+    // front still moves through the queue in order.
+    const unsigned int K = a.nreqs ? 16u : 1u;
+    const unsigned int groups = (a.total_tiles + K - 1) / K;
+    const unsigned int my_groups = pipe < groups ? (groups - 1 - pipe) / npipes + 1 : 0u;
+    unsigned int count = my_groups * K;
+    if (my_groups && pipe + (my_groups - 1) * npipes == groups - 1)
+      count -= groups * K - a.total_tiles;   // this pipe owns the partial last group
+    auto tile_of = [&](unsigned int i) { return ((i / K) * npipes + pipe) * K + i % K; };
     Tile tiles[kMaxStages];
     // batched drain: a tile is credited to its request(s) only once its bulk
     // store has COMPLETED; credits lag the stores by kCreditLag groups so the
@@ -524,7 +544,7 @@ pull_kernel_tma(const __grid_constant__ PullParams<MAXR> P, unsigned int stages)
     Tile pend[kCreditLag + 1];
     Credit cr;
     for (unsigned int k = 0; k < S && k < count; ++k) {
-      tiles[k] = audited(a, tile_at(a, runs, pipe + k * npipes), pipe + k * npipes);
+      tiles[k] = audited(a, tile_at(a, runs, tile_of(k)), tile_of(k));
       tma_load(ring + (size_t)k * a.tile_bytes, tiles[k].src, tiles[k].skip ? 0u : tiles[k].bytes,
                &bar[k]);
     }
@@ -539,7 +559,7 @@ pull_kernel_tma(const __grid_constant__ PullParams<MAXR> P, unsigned int stages)
         // refill the stage of tile i-1 with tile i-1+S
         const unsigned int k = i - 1 + S;
         if (k < count) {
-          tiles[sp] = audited(a, tile_at(a, runs, pipe + k * npipes), pipe + k * npipes);
+          tiles[sp] = audited(a, tile_at(a, runs, tile_of(k)), tile_of(k));
           tma_load(ring + (size_t)sp * a.tile_bytes, tiles[sp].src,
                    tiles[sp].skip ? 0u : tiles[sp].bytes, &bar[sp]);
         }
