@@ -265,18 +265,23 @@ def test_completion_flag_never_precedes_data():
         pair.close()
 
 
-@pytest.mark.parametrize("single_allocation", [False, True])
-def test_c2_full_size_sampled(single_allocation):
+@pytest.mark.parametrize("single_allocation,devs", [(False, (0, 0)), (True, (0, 0)),
+                                                    (False, (0, 1))])
+def test_c2_full_size_sampled(single_allocation, devs):
     """C2 at full size (32 layers x 32 heads x 128, 8K tokens = 4 GiB) in the
-    launch configuration bench.py times; checked on sampled elements
-    against the oracle's element addresses, plus a whole-request property
-    check (every pulled block equals its source block) on the device."""
+    launch configurations bench.py times (N = 1 loopback: LSU; N >= 2 over
+    NVLink: the auto TMA ring); checked on sampled elements against the
+    oracle's element addresses, plus a whole-request property check (every
+    pulled block equals its source block) on the device."""
     from gpu_helpers import cache_for
     from oracle import oracle
+    if max(devs) >= torch.cuda.device_count():
+        pytest.skip("needs two GPUs")
     g = kvdgen.C2
     n = kvdgen.blocks_for(kvdgen.C2_TOKENS, g.block_size)
-    src = cache_for(g, 0, single_allocation)
-    dst = cache_for(g, 0, single_allocation)
+    src = cache_for(g, devs[0], single_allocation)
+    dst = cache_for(g, devs[1], single_allocation)
+    ddev = torch.device("cuda", devs[1])
     for l in range(g.num_layers):
         kvdgen.torch_fill_random_(src.layers[l], 1000 + l)
         kvdgen.torch_fill_random_(dst.layers[l], 2000 + l)
@@ -286,13 +291,14 @@ def test_c2_full_size_sampled(single_allocation):
         rng = np.random.default_rng(5)
         untouched = np.setdiff1d(np.arange(g.num_blocks), d_ids)[:16]
         span = src.span_bytes
-        before = {l: dst.layers[l].view(2, g.num_blocks, span)[:, torch.from_numpy(untouched).long().cuda()].cpu()
+        before = {l: dst.layers[l].view(2, g.num_blocks, span)[:, torch.from_numpy(untouched).long().to(ddev)].cpu()
                   for l in (0, g.num_layers - 1)}
         rid = next_request_id()
         peer.pull(rid, s_ids, d_ids)
         peer.wait(rid)
         info = peer.info()
         assert info["bytes"] == 4 * 2**30
+        assert info["variant"] == (4 if devs[0] != devs[1] else 2)   # the bench's movers
         # sampled elements, addresses from the oracle's dot product
         e = g.elem_bytes
         for _ in range(2000):
@@ -303,15 +309,15 @@ def test_c2_full_size_sampled(single_allocation):
                                                int(s_ids[i]), kv, t, h, d)
             do = oracle.c_layer_element_offset((0,) * 5, g.num_blocks, 16, 32, 128, e,
                                                int(d_ids[i]), kv, t, h, d)
-            assert torch.equal(dst.layers[l][do:do + e], src.layers[l][so:so + e])
+            assert torch.equal(dst.layers[l][do:do + e].cpu(), src.layers[l][so:so + e].cpu())
         # whole request on device + untouched blocks
-        si = torch.from_numpy(s_ids).long().cuda()
-        di = torch.from_numpy(d_ids).long().cuda()
+        si = torch.from_numpy(s_ids).long().to(src.layers[0].device)
+        di = torch.from_numpy(d_ids).long().to(ddev)
         for l in range(g.num_layers):
             assert torch.equal(dst.layers[l].view(2, g.num_blocks, span)[:, di],
-                               src.layers[l].view(2, g.num_blocks, span)[:, si]), l
+                               src.layers[l].view(2, g.num_blocks, span)[:, si].to(ddev)), l
         for l, b in before.items():
-            now = dst.layers[l].view(2, g.num_blocks, span)[:, torch.from_numpy(untouched).long().cuda()].cpu()
+            now = dst.layers[l].view(2, g.num_blocks, span)[:, torch.from_numpy(untouched).long().to(ddev)].cpu()
             assert torch.equal(now, b)
     finally:
         peer.close()
