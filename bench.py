@@ -181,13 +181,40 @@ def cpu_oracle_sample(target_s: float = 12.0):
         assert rc == 0
         return dt, k * g.num_layers * 2 * g.block_size * g.num_kv_heads * g.head_dim * 2
 
+    def run_all_cores(k, threads):
+        """The same oracle call, one host thread per group of layers (ctypes
+        releases the GIL inside the C loop): the oracle as it stands, on every
+        core of the box."""
+        from concurrent.futures import ThreadPoolExecutor
+        nb = 2 * k
+        lb = oracle.layer_nbytes((0,) * 5, nb, g.block_size, g.num_kv_heads, g.head_dim, 2)
+        src = [kvdgen.random_bytes(lb, 10 + l) for l in range(g.num_layers)]
+        dst = [np.zeros(lb, np.uint8) for _ in range(g.num_layers)]
+        s, d = kvdgen.fragmented_table(k, nb, nb, seed=2)
+        groups = [list(range(i, g.num_layers, threads)) for i in range(threads)]
+        groups = [x for x in groups if x]
+
+        def part(ls):
+            return oracle.pull([src[l] for l in ls], (0,) * 5, nb, [dst[l] for l in ls], (0,) * 5,
+                               nb, g.num_kv_heads, g.head_dim, g.block_size, 2, s, d)
+        t = time.perf_counter()
+        with ThreadPoolExecutor(len(groups)) as ex:
+            assert all(rc == 0 for rc in ex.map(part, groups))
+        dt = time.perf_counter() - t
+        return dt, k * g.num_layers * 2 * g.block_size * g.num_kv_heads * g.head_dim * 2, len(groups)
+
     dt, b = run(2)
     k = int(max(2, min(256, 2 * target_s / max(dt, 1e-3))))
     dt, b = run(k)
+    ncpu = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    adt, ab, used = run_all_cores(k, min(ncpu, g.num_layers))
     return {"value": round(b / dt / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
             "seconds": round(dt, 2),
             "sample": f"C2 geometry, fragmented {k}-block request ({b / 2**20:.0f} MiB) from "
-                      f"{2 * k}-block pools, oracle/kvd_oracle.c element loop, 1 thread"}
+                      f"{2 * k}-block pools, oracle/kvd_oracle.c element loop, 1 thread",
+            "all_cores": {"value": round(ab / adt / 1e9, 4), "unit": "GB/s", "cores": used,
+                          "seconds": round(adt, 2),
+                          "what": "same sample, layers split over host threads"}}
 
 
 # ---------------------------------------------------------------------------
@@ -492,6 +519,9 @@ def run_kvd(args, rank, world, local_rank):
     barrier()
     timed_launches = launches[0]
     kern_ms_total, kern_launches = peer.kernel_time() if peer else (0.0, 0)
+    # %globaltimer cross-check (first CTA start -> last CTA done, single pulls
+    # only; batches have no whole-launch arrival)
+    gt_ms_total, gt_launches = peer.device_time() if peer else (0.0, 0)
     if peer:
         peer.set(kvd.OPT_TIMING, 0)
     # Per-request transfer latency (R16): issue -> completion observed, one
@@ -565,6 +595,8 @@ def run_kvd(args, rank, world, local_rank):
              "bytes": bytes_per_step * K if peer else 0,
              "step_ms": float(np.mean(step_ms)) if step_ms else 0.0,
              "kern_ms": kern_ms_total / K if peer else 0.0, "kern_launches": kern_launches,
+             "gt_ms": gt_ms_total / gt_launches if gt_launches else 0.0,
+             "gt_ms_total": gt_ms_total, "gt_launches": gt_launches,
              "lat": lat_ns, "clock": sampler.summary(), "info": info, "base": base,
              "launches": timed_launches, "runs": info.get("runs"), "ce_gbs": ce_gbs,
              "bytes_per_step": bytes_per_step if peer else 0}
@@ -595,6 +627,13 @@ def run_kvd(args, rank, world, local_rank):
                     "algorithmic_bytes_per_step": bytes_per_step,
                     "per_pair_achieved": [round(x, 1) for x in per_pair],
                     "traffic": traffic_from_profile(args.config, True)}
+            if all(s["gt_launches"] for s in dec):
+                gt = [s["bytes"] / (s["gt_ms_total"] / 1e3) / 1e9 for s in dec]
+                roof["globaltimer_cross_check"] = {
+                    "achieved": round(float(np.mean(gt)), 1),
+                    "ms_per_launch": round(float(np.mean([s["gt_ms"] for s in dec])), 4),
+                    "what": "in-kernel %globaltimer, first CTA start -> last CTA done, "
+                            "averaged over the timed launches (no launch latency)"}
         else:
             alg = 2 * bytes_per_step   # loopback: every byte is read and written in the same HBM
             roof = {"bound": "hbm", "achieved": round(alg / (kern_dev / 1e3) / 1e9, 1),
@@ -603,6 +642,13 @@ def run_kvd(args, rank, world, local_rank):
                     "peak_source": peak_src + " hbm_gbs (burst copy, read+write bytes)",
                     "algorithmic_bytes_per_step": alg,
                     "traffic": traffic_from_profile(args.config, False)}
+            s0 = dec[0]
+            if s0["gt_launches"]:
+                roof["globaltimer_cross_check"] = {
+                    "achieved": round(2 * s0["bytes"] / (s0["gt_ms_total"] / 1e3) / 1e9, 1),
+                    "ms_per_launch": round(s0["gt_ms"], 4),
+                    "what": "in-kernel %globaltimer, first CTA start -> last CTA done, "
+                            "averaged over the timed launches (no launch latency)"}
         clk = all_stats[world // 2 if multi else 0]["clock"]
         out = {
             "metric": METRIC, "value": round(total / t_dev / 1e9, 2), "unit": "GB/s",

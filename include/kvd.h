@@ -115,8 +115,10 @@ typedef struct {
 } kvd_pull_info;
 
 typedef enum {
-  KVD_VARIANT_AUTO = 0,  /* library choice */
-  KVD_VARIANT_LSU = 1,   /* SM loads 16 B/lane from the peer, stores locally (default) */
+  KVD_VARIANT_AUTO = 0,  /* default: the library's choice -- the TMA ring over NVLink, LSU32
+                            for loopback, requests <= 2 MiB and batches of short requests
+                             */
+  KVD_VARIANT_LSU = 1,   /* SM loads 16 B/lane from the peer, stores locally */
   KVD_VARIANT_LSU32 = 2, /* 32 B/lane (sm_100 256-bit ld/st); needs 32 B alignment */
   KVD_VARIANT_CE = 3,    /* copy engine: one cudaMemcpyAsync per segment (comparator only) */
   KVD_VARIANT_TMA = 4    /* one lane per warp runs an S-stage cp.async.bulk ring peer HBM ->
@@ -125,18 +127,22 @@ typedef enum {
 
 typedef enum {
   KVD_OPT_MAX_CTAS = 0,     /* cap on the pull grid (default: SMs * resident CTAs/SM) */
-  KVD_OPT_TILE_BYTES = 1,   /* bytes per warp work item, multiple of 512 (default 16384) */
+  KVD_OPT_TILE_BYTES = 1,   /* bytes per warp work item, multiple of 512 (default: auto policy;
+                               16384 for an explicit variant) */
   KVD_OPT_COALESCE = 2,     /* 1 (default) merge bi-contiguous runs; 0 one run per block (E10 ablation) */
   KVD_OPT_VARIANT = 3,      /* kvd_variant */
   KVD_OPT_THREADS = 4,      /* threads per CTA: multiple of 32; LSU 32..512 (default 512);
-                               TMA: threads/32 pipes per CTA, 32..256 (default 96) */
-  KVD_OPT_STAGES = 5,       /* TMA ring depth per pipe, 2..8 (default 4); pipes * stages *
+                               TMA: threads/32 pipes per CTA, 32..256 (default 96 for an
+                               explicit TMA variant; the auto policy picks its own) */
+  KVD_OPT_STAGES = 5,       /* TMA ring depth per pipe, 2..8 (default 4; auto: 6 or 3); pipes * stages *
                                tile_bytes must fit in 225 KiB of shared memory */
   KVD_OPT_AUDIT = 6,        /* 1: every tile checks that it stays inside its layer tensors on
                                both sides; violations are counted (kvd_peer_audit) and not
                                copied.  A test/debug mode; 0 (default) off */
   KVD_OPT_TIMING = 7        /* 1: record CUDA events right around every pull kernel on the
-                               caller's stream; kvd_peer_kernel_time sums them.  0 (default) off */
+                               caller's stream (kvd_peer_kernel_time sums them) and have single
+                               pulls measure first-CTA-start -> last-CTA-done with %globaltimer
+                               (kvd_peer_device_time).  0 (default) off */
 } kvd_option;
 
 typedef struct kvd_cache_s* kvd_cache;
@@ -346,6 +352,13 @@ KVD_API kvd_status kvd_peer_audit(kvd_peer peer, uint64_t* violations);
  * (KVD_OPT_TIMING): waits for them, returns the summed milliseconds and the
  * number of launches, and forgets them.  KVD_ESTATE if timing is off. */
 KVD_API kvd_status kvd_peer_kernel_time(kvd_peer peer, double* total_ms, uint64_t* launches);
+
+/* In-kernel duration (KVD_OPT_TIMING, single pulls, SURVEY §8 d's
+ * %globaltimer cross-check): the summed nanosecond-timer spans from the
+ * first CTA's start to the last CTA's completion, over the requests retired
+ * by kvd_poll_done / kvd_wait_done since the previous call, in ms, and their
+ * count; then resets.  Unlike the events it excludes launch latency. */
+KVD_API kvd_status kvd_peer_device_time(kvd_peer peer, double* total_ms, uint64_t* launches);
 
 /* Describe the most recent kvd_pull on this peer. */
 KVD_API kvd_status kvd_last_pull_info(kvd_peer peer, kvd_pull_info* out);

@@ -478,6 +478,7 @@ struct kvd_peer_s {
     uint32_t slot;
     uint64_t token;
     int32_t batch;                          // batch descriptor buffer, -1 for single pulls
+    bool timed = false;                     // the kernel writes its %globaltimer duration
   };
   std::unordered_map<uint64_t, InFlight> inflight;
   unsigned long long* bytectr = nullptr;    // device per-slot byte counters (batched drain)
@@ -512,6 +513,11 @@ struct kvd_peer_s {
   bool closed = false;
   unsigned int* audit_ctr = nullptr;        // KVD_OPT_AUDIT violation counter (device)
   bool timing = false;                      // KVD_OPT_TIMING
+  unsigned long long* gt_start = nullptr;   // per-slot earliest CTA start (device, ~0 idle)
+  unsigned long long* gt_host = nullptr;    // per-slot duration ns (pinned, host-mapped)
+  unsigned long long* gt_dev = nullptr;
+  double gt_total_ms = 0;                   // durations of retired timed requests
+  uint64_t gt_count = 0;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed, event_pool;
   // §8 f4 head-sliced peer (row_bytes > 0): remote unit = block_size rows
   uint32_t row_bytes = 0;
@@ -836,6 +842,8 @@ static void peer_release(kvd_peer p) {
   if (p->counters) cudaFree(p->counters);
   if (p->bytectr) cudaFree(p->bytectr);
   if (p->audit_ctr) cudaFree(p->audit_ctr);
+  if (p->gt_start) cudaFree(p->gt_start);
+  if (p->gt_host) cudaFreeHost(p->gt_host);
   for (auto* v : {&p->timed, &p->event_pool})
     for (auto& ev : *v) {
       cudaEventDestroy(ev.first);
@@ -970,6 +978,12 @@ static kvd_status open_impl(kvd_cache local, const void* blob, size_t blob_len,
   KVD_CUDA(cudaMemset(p->counters, 0, kSlots * sizeof(unsigned int)));
   KVD_CUDA(cudaMalloc(&p->bytectr, kSlots * sizeof(unsigned long long)));
   KVD_CUDA(cudaMemset(p->bytectr, 0, kSlots * sizeof(unsigned long long)));
+  KVD_CUDA(cudaMalloc(&p->gt_start, kSlots * sizeof(unsigned long long)));
+  KVD_CUDA(cudaMemset(p->gt_start, 0xff, kSlots * sizeof(unsigned long long)));
+  KVD_CUDA(cudaHostAlloc((void**)&p->gt_host, kSlots * sizeof(unsigned long long),
+                         cudaHostAllocMapped | cudaHostAllocPortable));
+  memset(p->gt_host, 0, kSlots * sizeof(unsigned long long));
+  KVD_CUDA(cudaHostGetDevicePointer((void**)&p->gt_dev, p->gt_host, 0));
   KVD_CUDA(cudaDeviceSynchronize());
   p->slot_seq.assign(kSlots, 0);
   p->slot_runs_dev.assign(kSlots, nullptr);
@@ -1249,6 +1263,11 @@ static kvd_status transfer(kvd_peer p, uint64_t request_id, const int32_t* src_i
   a.audit = p->audit_ctr;
   a.src_layer_bytes = sg.layer_bytes;
   a.dst_layer_bytes = dg_.layer_bytes;
+  const bool timed = p->timing && n > 0 && variant != KVD_VARIANT_CE;
+  if (timed) {
+    a.gt_start = p->gt_start + slot;
+    a.gt_out = p->gt_dev + slot;
+  }
 
   DeviceGuard dgd(p->local->device);
   if (!dgd.ok) return fail(KVD_ECUDA, "cannot select device %d", p->local->device);
@@ -1320,7 +1339,7 @@ static kvd_status transfer(kvd_peer p, uint64_t request_id, const int32_t* src_i
   info.variant = (uint32_t)variant;
   p->slot_seq[slot] = token;
   p->cursor = (slot + 1) % kSlots;
-  p->inflight[request_id] = kvd_peer_s::InFlight{slot, token, -1};
+  p->inflight[request_id] = kvd_peer_s::InFlight{slot, token, -1, timed};
   p->last = info;
   return KVD_OK;
 }
@@ -1503,6 +1522,10 @@ kvd_status kvd_poll_done(kvd_peer p, uint64_t request_id, int* done) {
   if (v == token) {
     *done = 1;
     p->slot_seq[slot] = 0;
+    if (it->second.timed) {   // written before the slot word's release
+      p->gt_total_ms += (double)__atomic_load_n(&p->gt_host[slot], __ATOMIC_RELAXED) * 1e-6;
+      ++p->gt_count;
+    }
     if (it->second.batch >= 0) --p->batch_bufs[it->second.batch].refs;
     p->inflight.erase(it);
   } else {
@@ -1593,6 +1616,16 @@ kvd_status kvd_peer_kernel_time(kvd_peer p, double* total_ms, uint64_t* launches
   *launches = p->timed.size();
   p->event_pool.insert(p->event_pool.end(), p->timed.begin(), p->timed.end());
   p->timed.clear();
+  return KVD_OK;
+}
+
+kvd_status kvd_peer_device_time(kvd_peer p, double* total_ms, uint64_t* launches) {
+  if (!p || !total_ms || !launches) return fail(KVD_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lk(p->mu);
+  *total_ms = p->gt_total_ms;
+  *launches = p->gt_count;
+  p->gt_total_ms = 0;
+  p->gt_count = 0;
   return KVD_OK;
 }
 

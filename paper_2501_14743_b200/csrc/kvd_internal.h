@@ -58,6 +58,12 @@ struct PullArgs {
   // lie inside their layer tensors, counts violations here and skips them.
   unsigned int* audit;
   unsigned long long src_layer_bytes, dst_layer_bytes;
+  // Device-side duration (KVD_OPT_TIMING, single pulls): every CTA
+  // atomicMin's its %globaltimer start into *gt_start (reset to ~0 by the
+  // last CTA); the last CTA writes end - start (ns) to *gt_out (pinned,
+  // host-mapped) before it releases the slot word.  nullptr: off.
+  unsigned long long* gt_start;
+  unsigned long long* gt_out;
 
   // TP-resharding (§8 f4): row_bytes > 0 makes every unit block_size rows
   // of row_bytes, src_row_stride / dst_row_stride apart, and shifts the

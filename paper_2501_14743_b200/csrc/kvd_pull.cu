@@ -96,6 +96,15 @@ __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned l
 __device__ __forceinline__ void fence_acq_rel_gpu() {
   asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// KVD_OPT_TIMING: the earliest CTA start of this launch (see PullArgs::gt_start)
+__device__ __forceinline__ void mark_start(const PullArgs& a) {
+  if (a.gt_start != nullptr && threadIdx.x == 0) atomicMin(a.gt_start, globaltimer());
+}
 
 // One warp copies `bytes` (multiple of sizeof(V)) from src to dst.  All U
 // loads of a batch are issued before any store so each lane keeps U
@@ -388,6 +397,11 @@ __device__ __forceinline__ void complete(const PullArgs& a) {
     if (prev == gridDim.x - 1) {
       *a.counter = 0u;
       fence_acq_rel_gpu();
+      if (a.gt_start != nullptr) {   // first CTA start -> last CTA done, before the release
+        const unsigned long long t1 = globaltimer();
+        *(volatile unsigned long long*)a.gt_out = t1 - *(volatile unsigned long long*)a.gt_start;
+        *a.gt_start = ~0ull;
+      }
       publish_token(a, a.flag, a.token, a.request_id);
     }
   }
@@ -416,6 +430,7 @@ __global__ void __launch_bounds__(512, 2)
 pull_kernel(const __grid_constant__ PullParams<MAXR> P) {
   extern __shared__ int4 s_runs[];
   const PullArgs& a = P.a;
+  mark_start(a);
   const int4* runs = stage_runs(a, (MAXR > 0) ? P.runs : a.runs_dev, s_runs);
   const unsigned int lane = threadIdx.x & 31u;
   const unsigned int warps_per_cta = blockDim.x >> 5;
@@ -506,6 +521,7 @@ pull_kernel_tma(const __grid_constant__ PullParams<MAXR> P, unsigned int stages)
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint64_t bars[(256 / 32) * kMaxStages];   // <= 8 pipes (launch bound)
   const PullArgs& a = P.a;
+  mark_start(a);
   const unsigned int warp = threadIdx.x >> 5;
   const unsigned int pipes_per_cta = blockDim.x >> 5;
   const unsigned int npipes = gridDim.x * pipes_per_cta;

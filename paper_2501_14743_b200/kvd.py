@@ -30,7 +30,8 @@ EXPORTED = (
     "kvd_open_peer_heads",
     "kvd_close_peer",
     "kvd_peer_set", "kvd_pull", "kvd_push", "kvd_pull_batch", "kvd_poll_done", "kvd_wait_done",
-    "kvd_last_pull_info", "kvd_peer_audit", "kvd_peer_kernel_time", "kvd_poll_released",
+    "kvd_last_pull_info", "kvd_peer_audit", "kvd_peer_kernel_time", "kvd_peer_device_time",
+    "kvd_poll_released",
     "kvd_gather", "kvd_scatter", "kvd_strerror", "kvd_last_error", "kvd_abi_version",
 )
 
@@ -108,6 +109,7 @@ _SIGS = {
     "kvd_peer_audit": [_p, ctypes.POINTER(_u64)],
     "kvd_poll_released": [_p, _p, _u32, ctypes.POINTER(_u32)],
     "kvd_peer_kernel_time": [_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_u64)],
+    "kvd_peer_device_time": [_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_u64)],
     "kvd_gather": [_p, _pi32, _u32, _p, _p],
     "kvd_scatter": [_p, _pi32, _u32, _p, _p],
 }
@@ -335,6 +337,14 @@ def kvd_peer_kernel_time(peer: int):
     ms, n = ctypes.c_double(0), _u64(0)
     _check(_lib.kvd_peer_kernel_time(peer, ctypes.byref(ms), ctypes.byref(n)),
            "kvd_peer_kernel_time")
+    return ms.value, n.value
+
+
+def kvd_peer_device_time(peer: int):
+    """(summed %globaltimer kernel spans in ms, requests) retired since the previous call."""
+    ms, n = ctypes.c_double(0), _u64(0)
+    _check(_lib.kvd_peer_device_time(peer, ctypes.byref(ms), ctypes.byref(n)),
+           "kvd_peer_device_time")
     return ms.value, n.value
 
 

@@ -146,6 +146,11 @@ class Peer:
         """(kernel-only ms summed, launches) since the last call; needs OPT_TIMING."""
         return kvd.kvd_peer_kernel_time(self.handle)
 
+    def device_time(self):
+        """(ms, requests): in-kernel first-CTA-start -> last-CTA-done spans of the
+        retired single pulls since the last call; needs OPT_TIMING."""
+        return kvd.kvd_peer_device_time(self.handle)
+
     def info(self) -> dict:
         return kvd.kvd_last_pull_info(self.handle).as_dict()
 

@@ -66,3 +66,29 @@ def test_over_nvlink_uses_tma_ring():
         assert_layers_equal(pair.download_dst(), pair.expected(s, d))
     finally:
         pair.close()
+
+
+def test_device_time_globaltimer_cross_check():
+    """KVD_OPT_TIMING: the in-kernel %globaltimer span (first CTA start ->
+    last CTA done) of each retired single pull, next to the CUDA-event time
+    around the launch (which also holds the launch latency)."""
+    from paper_2501_14743_b200 import kvd
+    pair = make_pair(G7B, G7B, seed=105)
+    try:
+        pair.peer.set(kvd.OPT_TIMING, 1)
+        s, d = kvdgen.fragmented_table(32, G7B.num_blocks, G7B.num_blocks, seed=6)
+        for _ in range(3):
+            pull_and_wait(pair, s, d)
+        gt_ms, n = pair.peer.device_time()
+        ev_ms, m = pair.peer.kernel_time()
+        assert n == 3 and m == 3
+        assert 0 < gt_ms <= ev_ms * 1.02, (gt_ms, ev_ms)
+        # 256 MiB each way through one HBM: no faster than ~10 TB/s of r+w
+        assert gt_ms / 3 > 2 * 32 * G7B.num_layers * 2 * (128 << 10) / 10e12 * 1e3
+        assert pair.peer.device_time() == (0.0, 0)              # reset by the read
+        pair.peer.set(kvd.OPT_TIMING, 0)
+        pull_and_wait(pair, s, d)
+        assert pair.peer.device_time() == (0.0, 0)              # off: nothing recorded
+        assert_layers_equal(pair.download_dst(), pair.expected(s, d))
+    finally:
+        pair.close()
