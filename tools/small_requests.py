@@ -90,6 +90,7 @@ def main():
         peer.set(kvd.OPT_STAGES, a.stages)
     if a.ctas:
         peer.set(kvd.OPT_MAX_CTAS, a.ctas)
+    peer.set(kvd.OPT_TIMING, 1)   # in-kernel %globaltimer spans of single pulls
     torch.cuda.set_device(a.dst_dev)
     stream = torch.cuda.Stream(a.dst_dev)
     rid = [0]
@@ -134,6 +135,11 @@ def main():
                 if it >= 2:
                     times.append(e0.elapsed_time(e1))
             ms = float(np.median(times))
+            gt_ms, gt_n = peer.device_time()
+            peer.kernel_time()
+            if gt_n:   # mean in-kernel span per request vs the per-request share of the step
+                res[mode + "_kernel_us_per_request"] = round(gt_ms / gt_n * 1e3, 2)
+                res[mode + "_step_us_per_request"] = round(ms * 1e3 / (len(tables) if mode == "single" else 1), 2)
             res[mode + "_ms"] = round(ms, 4)
             res[mode + "_gbs"] = round(nbytes / ms / 1e6, 1)
             res[mode + "_info"] = {k: peer.info()[k] for k in ("variant", "ctas", "threads", "runs")}
