@@ -269,11 +269,17 @@ __device__ __forceinline__ bool tile_in_bounds(const PullArgs& a, const Tile& T,
 // claim's NVLink round trip (~1.5 us) overlaps the host-flag release that
 // sits between them (fence_probe: 4.5 -> 3.1 us for the whole sequence).
 __device__ __forceinline__ unsigned long long mbox_claim(const PullArgs& a) {
+#ifdef KVD_EXPERIMENT_NO_MBOX   // A/B experiment only: no prefill notification
+  return 0ull;
+#endif
   return a.mbox ? atomicAdd_system(a.mbox, 1ull) : 0ull;
 }
 __device__ __forceinline__ void mbox_post(const PullArgs& a, unsigned long long s,
                                           unsigned long long request_id) {
   if (a.mbox == nullptr) return;
+#ifdef KVD_EXPERIMENT_NO_MBOX
+  return;
+#endif
   unsigned long long* e = a.mbox + 8 + 2 * (s % kReleaseRing);
   *(volatile unsigned long long*)(e + 1) = request_id;
   st_release_sys(e, s + 1);
