@@ -433,6 +433,8 @@ def run_kvd(args, rank, world, local_rank):
             peer.set(kvd.OPT_MAX_CTAS, args.max_ctas)
         if args.no_coalesce:
             peer.set(kvd.OPT_COALESCE, 0)
+        if args.streams:
+            peer.set(kvd.OPT_STREAMS, args.streams)
 
     stream = torch.cuda.Stream(dev)
     rid = [rank * 10_000_000]
@@ -509,9 +511,11 @@ def run_kvd(args, rank, world, local_rank):
         if peer:
             t_start.record(stream)
             for k in range(K):
-                issue(ev[k])
+                issue(ev[k] if not args.streams else None)
                 if len(pending) > 768:
                     retire(512)
+            if args.streams:
+                peer.stream_wait(stream)   # join the library streams before the end event
             t_end.record(stream)
             retire(0)
         torch.cuda.synchronize()
@@ -529,10 +533,13 @@ def run_kvd(args, rank, world, local_rank):
     if peer:
         for _ in range(max(3, min(K, 50 if n_req == 1 else 5))):
             step(lat_ns)
+        if args.streams:
+            peer.set(kvd.OPT_STREAMS, 0)   # parity check and calibration in stream order
 
     info = peer.info() if peer else {}
     dev_s = t_start.elapsed_time(t_end) / 1e3 if peer else 0.0
-    step_ms = [a.elapsed_time(b) for a, b in ev]
+    step_ms = ([a.elapsed_time(b) for a, b in ev] if not args.streams
+               else [dev_s * 1e3 / K] if peer else [])
     span = (src or dst).span_bytes
     bytes_per_step = n_blocks * g.num_layers * 2 * span
 
@@ -666,8 +673,10 @@ def run_kvd(args, rank, world, local_rank):
                             "no NVLink pair)") if not multi else
                            f"{pairs}P:{pairs}D rail pairs, rank k -> rank {pairs}+k over NVLink 5",
                 "parallelism": "loopback" if not multi else f"{pairs}x(1P:1D)",
-                "issue": "kvd_pull_batch (one launch per step)" if args.batch
-                         else "one kvd_pull per request",
+                "issue": ("kvd_pull_batch (one launch per step)" if args.batch
+                          else "one kvd_pull per request")
+                         + (f"; KVD_OPT_STREAMS={args.streams} (consecutive launches overlap "
+                            "on library streams)" if args.streams else "; stream-ordered"),
                 "l2": "no flush: every step moves >= 640 MiB per pair, >> 126 MB L2",
                 "cache_dtype": "fp16" if g.dtype == kvdgen.FP16 else "bf16",
                 "variant": info0.get("variant"), "ctas": info0.get("ctas"),
@@ -752,6 +761,9 @@ def main():
     ap.add_argument("--threads", type=int, default=0)
     ap.add_argument("--max-ctas", type=int, default=0)
     ap.add_argument("--no-coalesce", action="store_true")
+    ap.add_argument("--streams", type=int, default=0,
+                    help="KVD_OPT_STREAMS: >= 2 lets consecutive pulls overlap on library "
+                         "streams (completion still polled per request)")
     ap.add_argument("--memory", choices=["torch", "vmm"], default="torch",
                     help="cache memory: torch/cudaMalloc (legacy IPC) or kvd_mem_alloc (VMM, "
                          "POSIX-fd/fabric handles, §8 f3 groundwork)")

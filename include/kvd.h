@@ -139,10 +139,19 @@ typedef enum {
   KVD_OPT_AUDIT = 6,        /* 1: every tile checks that it stays inside its layer tensors on
                                both sides; violations are counted (kvd_peer_audit) and not
                                copied.  A test/debug mode; 0 (default) off */
-  KVD_OPT_TIMING = 7        /* 1: record CUDA events right around every pull kernel on the
+  KVD_OPT_TIMING = 7,       /* 1: record CUDA events right around every pull kernel on the
                                caller's stream (kvd_peer_kernel_time sums them) and have single
                                pulls measure first-CTA-start -> last-CTA-done with %globaltimer
                                (kvd_peer_device_time).  0 (default) off */
+  KVD_OPT_STREAMS = 8       /* 0 or 1 (default): every transfer runs on the caller's stream, in
+                               stream order.  k in [2, 8]: a transfer still waits for the work
+                               already on the caller's stream, but runs on the next of k library
+                               streams, so consecutive transfers overlap (their launch, ramp and
+                               completion tails hide behind each other); the caller's stream does
+                               NOT wait for it -- observe completion with kvd_poll_done /
+                               kvd_wait_done (the paper's decode worker polls) or order a
+                               stream after it with kvd_stream_wait.  Changing it synchronises the
+                               library streams */
 } kvd_option;
 
 typedef struct kvd_cache_s* kvd_cache;
@@ -359,6 +368,12 @@ KVD_API kvd_status kvd_peer_kernel_time(kvd_peer peer, double* total_ms, uint64_
  * by kvd_poll_done / kvd_wait_done since the previous call, in ms, and their
  * count; then resets.  Unlike the events it excludes launch latency. */
 KVD_API kvd_status kvd_peer_device_time(kvd_peer peer, double* total_ms, uint64_t* launches);
+
+/* KVD_OPT_STREAMS >= 2: make `stream` (of the peer's local device) wait for
+ * every transfer issued on this peer so far.  A no-op otherwise (transfers
+ * are then already in the caller's stream order).  Errors: KVD_EINVAL,
+ * KVD_ECUDA. */
+KVD_API kvd_status kvd_stream_wait(kvd_peer peer, void* stream);
 
 /* Describe the most recent kvd_pull on this peer. */
 KVD_API kvd_status kvd_last_pull_info(kvd_peer peer, kvd_pull_info* out);

@@ -518,6 +518,12 @@ struct kvd_peer_s {
   unsigned long long* gt_dev = nullptr;
   double gt_total_ms = 0;                   // durations of retired timed requests
   uint64_t gt_count = 0;
+  // KVD_OPT_STREAMS >= 2: transfers fork off the caller's stream onto these
+  uint32_t nstreams = 0;
+  std::vector<cudaStream_t> streams;
+  std::vector<cudaEvent_t> join_events;     // one per library stream (kvd_stream_wait)
+  cudaEvent_t fork_event = nullptr;
+  uint32_t next_stream = 0;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed, event_pool;
   // §8 f4 head-sliced peer (row_bytes > 0): remote unit = block_size rows
   uint32_t row_bytes = 0;
@@ -844,6 +850,9 @@ static void peer_release(kvd_peer p) {
   if (p->audit_ctr) cudaFree(p->audit_ctr);
   if (p->gt_start) cudaFree(p->gt_start);
   if (p->gt_host) cudaFreeHost(p->gt_host);
+  for (auto s : p->streams) cudaStreamDestroy(s);
+  for (auto e : p->join_events) cudaEventDestroy(e);
+  if (p->fork_event) cudaEventDestroy(p->fork_event);
   for (auto* v : {&p->timed, &p->event_pool})
     for (auto& ev : *v) {
       cudaEventDestroy(ev.first);
@@ -1050,6 +1059,33 @@ kvd_status kvd_peer_set(kvd_peer p, int option, int64_t value) {
     case KVD_OPT_TIMING:
       p->timing = value != 0;
       return KVD_OK;
+    case KVD_OPT_STREAMS: {
+      if (value < 0 || value > 8) return fail(KVD_EINVAL, "streams must be in [0, 8]");
+      const uint32_t k = value < 2 ? 0u : (uint32_t)value;
+      if (k == p->nstreams) return KVD_OK;
+      DeviceGuard dg(p->local->device);
+      if (!dg.ok) return fail(KVD_ECUDA, "cannot select device %d", p->local->device);
+      for (auto s : p->streams) {          // transfers already forked finish first
+        cudaStreamSynchronize(s);
+        cudaStreamDestroy(s);
+      }
+      for (auto e : p->join_events) cudaEventDestroy(e);
+      p->streams.clear();
+      p->join_events.clear();
+      p->next_stream = 0;
+      p->nstreams = k;
+      if (k && !p->fork_event)
+        KVD_CUDA(cudaEventCreateWithFlags(&p->fork_event, cudaEventDisableTiming));
+      for (uint32_t i = 0; i < k; ++i) {
+        cudaStream_t s;
+        cudaEvent_t e;
+        KVD_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        p->streams.push_back(s);
+        KVD_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        p->join_events.push_back(e);
+      }
+      return KVD_OK;
+    }
     case KVD_OPT_AUDIT: {
       DeviceGuard dg(p->local->device);
       if (!dg.ok) return fail(KVD_ECUDA, "cannot select device %d", p->local->device);
@@ -1190,6 +1226,23 @@ static void head_slice_plan(const kvd_peer_s* p, const kvd_geometry& sg, PairPla
 }
 
 // KVD_OPT_TIMING: CUDA events right around a pull kernel on its stream.
+// KVD_OPT_STREAMS >= 2: order the transfer after everything already on the
+// caller's stream, then run it on the next library stream in turn, so
+// consecutive transfers overlap (the caller's stream does not wait for it;
+// kvd_stream_wait or the completion words order later work).
+static cudaError_t route_stream(kvd_peer_s* p, cudaStream_t user, cudaStream_t* out) {
+  *out = user;
+  if (p->streams.empty()) return cudaSuccess;
+  cudaError_t e = cudaEventRecord(p->fork_event, user);
+  if (e != cudaSuccess) return e;
+  cudaStream_t s = p->streams[p->next_stream];
+  e = cudaStreamWaitEvent(s, p->fork_event, 0);   // snapshots the event: reusable at once
+  if (e != cudaSuccess) return e;
+  p->next_stream = (p->next_stream + 1) % (uint32_t)p->streams.size();
+  *out = s;
+  return cudaSuccess;
+}
+
 static void timing_begin(kvd_peer_s* p, cudaStream_t s) {
   if (!p->timing) return;
   std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
@@ -1271,7 +1324,8 @@ static kvd_status transfer(kvd_peer p, uint64_t request_id, const int32_t* src_i
 
   DeviceGuard dgd(p->local->device);
   if (!dgd.ok) return fail(KVD_ECUDA, "cannot select device %d", p->local->device);
-  cudaStream_t stream = (cudaStream_t)stream_;
+  cudaStream_t stream = nullptr;
+  KVD_CUDA(route_stream(p, (cudaStream_t)stream_, &stream));
   kvd_pull_info info{};
   info.request_id = request_id;
   info.blocks = n;
@@ -1465,7 +1519,8 @@ kvd_status kvd_pull_batch(kvd_peer p, uint32_t num_requests, const uint64_t* req
       pos += p->runs[r].len;
     }
   }
-  cudaStream_t stream = (cudaStream_t)stream_;
+  cudaStream_t stream = nullptr;
+  KVD_CUDA(route_stream(p, (cudaStream_t)stream_, &stream));
   KVD_CUDA(cudaMemcpyAsync(B.dev, B.host, bytes_needed, cudaMemcpyHostToDevice, stream));
   a.runs_dev = reinterpret_cast<const int4*>(B.dev);
   a.nreqs = num_requests;
@@ -1616,6 +1671,19 @@ kvd_status kvd_peer_kernel_time(kvd_peer p, double* total_ms, uint64_t* launches
   *launches = p->timed.size();
   p->event_pool.insert(p->event_pool.end(), p->timed.begin(), p->timed.end());
   p->timed.clear();
+  return KVD_OK;
+}
+
+kvd_status kvd_stream_wait(kvd_peer p, void* stream) {
+  if (!p) return fail(KVD_EINVAL, "null peer");
+  std::lock_guard<std::mutex> lk(p->mu);
+  if (p->streams.empty()) return KVD_OK;   // transfers already run on the caller's streams
+  DeviceGuard dg(p->local->device);
+  if (!dg.ok) return fail(KVD_ECUDA, "cannot select device %d", p->local->device);
+  for (size_t i = 0; i < p->streams.size(); ++i) {
+    KVD_CUDA(cudaEventRecord(p->join_events[i], p->streams[i]));
+    KVD_CUDA(cudaStreamWaitEvent((cudaStream_t)stream, p->join_events[i], 0));
+  }
   return KVD_OK;
 }
 

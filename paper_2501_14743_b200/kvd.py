@@ -22,7 +22,7 @@ FP16, BF16, FP8, FP32 = 0, 1, 2, 3
 VARIANT_AUTO, VARIANT_LSU, VARIANT_LSU32, VARIANT_CE, VARIANT_TMA = 0, 1, 2, 3, 4
 MEM_AUTO, MEM_POSIX_FD, MEM_FABRIC = 0, 1, 8
 OPT_MAX_CTAS, OPT_TILE_BYTES, OPT_COALESCE, OPT_VARIANT, OPT_THREADS, OPT_STAGES = 0, 1, 2, 3, 4, 5
-OPT_AUDIT, OPT_TIMING = 6, 7
+OPT_AUDIT, OPT_TIMING, OPT_STREAMS = 6, 7, 8
 
 EXPORTED = (
     "kvd_layout_geometry", "kvd_plan", "kvd_blob_info", "kvd_register_cache",
@@ -31,6 +31,7 @@ EXPORTED = (
     "kvd_close_peer",
     "kvd_peer_set", "kvd_pull", "kvd_push", "kvd_pull_batch", "kvd_poll_done", "kvd_wait_done",
     "kvd_last_pull_info", "kvd_peer_audit", "kvd_peer_kernel_time", "kvd_peer_device_time",
+    "kvd_stream_wait",
     "kvd_poll_released",
     "kvd_gather", "kvd_scatter", "kvd_strerror", "kvd_last_error", "kvd_abi_version",
 )
@@ -110,6 +111,7 @@ _SIGS = {
     "kvd_poll_released": [_p, _p, _u32, ctypes.POINTER(_u32)],
     "kvd_peer_kernel_time": [_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_u64)],
     "kvd_peer_device_time": [_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_u64)],
+    "kvd_stream_wait": [_p, _p],
     "kvd_gather": [_p, _pi32, _u32, _p, _p],
     "kvd_scatter": [_p, _pi32, _u32, _p, _p],
 }
@@ -346,6 +348,11 @@ def kvd_peer_device_time(peer: int):
     _check(_lib.kvd_peer_device_time(peer, ctypes.byref(ms), ctypes.byref(n)),
            "kvd_peer_device_time")
     return ms.value, n.value
+
+
+def kvd_stream_wait(peer: int, stream: int) -> None:
+    """KVD_OPT_STREAMS >= 2: order `stream` after every transfer issued on the peer."""
+    _check(_lib.kvd_stream_wait(peer, stream), "kvd_stream_wait")
 
 
 def kvd_last_pull_info(peer: int) -> kvd_pull_info:

@@ -151,6 +151,11 @@ class Peer:
         retired single pulls since the last call; needs OPT_TIMING."""
         return kvd.kvd_peer_device_time(self.handle)
 
+    def stream_wait(self, stream: Optional[torch.cuda.Stream] = None) -> None:
+        """With OPT_STREAMS >= 2: order `stream` after every transfer issued so far."""
+        s = stream if stream is not None else torch.cuda.current_stream(self.local.device)
+        kvd.kvd_stream_wait(self.handle, s.cuda_stream)
+
     def info(self) -> dict:
         return kvd.kvd_last_pull_info(self.handle).as_dict()
 

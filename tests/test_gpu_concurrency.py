@@ -102,3 +102,43 @@ def test_slot_exhaustion_and_recovery():
         pair.peer.wait(rid)
     finally:
         pair.close()
+
+
+def test_library_streams_overlap_and_order():
+    """KVD_OPT_STREAMS = 2: transfers fork off the caller's stream (after the
+    work already queued there) onto library streams; kvd_stream_wait joins
+    them back.  Bytes stay the oracle's."""
+    from paper_2501_14743_b200 import kvd
+    pair = make_pair(G, G, seed=73)
+    try:
+        pair.peer.set(kvd.OPT_STREAMS, 2)
+        user = torch.cuda.Stream()
+        tables = kvdgen.disjoint_fragmented_tables([40, 33, 51, 20, 64], 512, 512, seed=7)
+        zero_host = [np.zeros_like(h) for h in pair.dst_host]
+        with torch.cuda.stream(user):
+            torch.cuda._sleep(200_000_000)                 # ~0.1 s: the pulls must wait for it
+            for t in pair.dst.layers:
+                t.zero_()                                   # ... and for this fill
+        rids = []
+        for s, d in tables:
+            rid = next_request_id()
+            pair.peer.pull(rid, s, d, user)
+            rids.append(rid)
+        pair.peer.stream_wait(user)                         # user stream after every pull
+        with torch.cuda.stream(user):
+            got = [t.clone() for t in pair.dst.layers]      # read on the user stream, no host poll
+        user.synchronize()
+        exp = zero_host
+        for s, d in tables:
+            exp = pair.expected(s, d, exp)
+        assert_layers_equal([g.cpu().numpy() for g in got], exp)
+        for rid in rids:
+            pair.peer.wait(rid)
+        assert sorted(pair.src.poll_released()) == sorted(rids)   # completion order may vary
+        pair.peer.set(kvd.OPT_STREAMS, 0)                   # back to stream order
+        s, d = kvdgen.disjoint_fragmented_tables([10], 512, 512, seed=8)[0]
+        rid = next_request_id()
+        pair.peer.pull(rid, s, d, user)
+        pair.peer.wait(rid)
+    finally:
+        pair.close()

@@ -93,6 +93,7 @@ def main():
     peer.set(kvd.OPT_TIMING, 1)   # in-kernel %globaltimer spans of single pulls
     torch.cuda.set_device(a.dst_dev)
     stream = torch.cuda.Stream(a.dst_dev)
+    stream2 = torch.cuda.Stream(a.dst_dev)
     rid = [0]
     for t in toks:
         n = kvdgen.blocks_for(t, g.block_size)
@@ -116,6 +117,20 @@ def main():
                         rid[0] += 1
                         peer.pull(rid[0], s, d, stream)
                         ids.append(rid[0])
+                elif mode == "lib2":   # KVD_OPT_STREAMS = 2: the library overlaps consecutive pulls
+                    peer.set(kvd.OPT_STREAMS, 2)
+                    for s, d in tables:
+                        rid[0] += 1
+                        peer.pull(rid[0], s, d, stream)
+                        ids.append(rid[0])
+                    peer.stream_wait(stream)
+                elif mode == "single2":   # alternate two streams: consecutive pulls may overlap
+                    stream2.wait_stream(stream)
+                    for k, (s, d) in enumerate(tables):
+                        rid[0] += 1
+                        peer.pull(rid[0], s, d, stream if k % 2 == 0 else stream2)
+                        ids.append(rid[0])
+                    stream.wait_stream(stream2)
                 elif mode == "batch1":   # the same blocks as a batch of ONE request
                     rid[0] += 1
                     peer.pull_batch([rid[0]], [merged], stream)
@@ -132,6 +147,8 @@ def main():
                 for r in ids:
                     peer.wait(r)
                 e1.synchronize()
+                if mode == "lib2":
+                    peer.set(kvd.OPT_STREAMS, 0)
                 if it >= 2:
                     times.append(e0.elapsed_time(e1))
             ms = float(np.median(times))
@@ -139,7 +156,8 @@ def main():
             peer.kernel_time()
             if gt_n:   # mean in-kernel span per request vs the per-request share of the step
                 res[mode + "_kernel_us_per_request"] = round(gt_ms / gt_n * 1e3, 2)
-                res[mode + "_step_us_per_request"] = round(ms * 1e3 / (len(tables) if mode == "single" else 1), 2)
+                res[mode + "_step_us_per_request"] = round(
+                    ms * 1e3 / (len(tables) if mode in ("single", "single2", "lib2") else 1), 2)
             res[mode + "_ms"] = round(ms, 4)
             res[mode + "_gbs"] = round(nbytes / ms / 1e6, 1)
             res[mode + "_info"] = {k: peer.info()[k] for k in ("variant", "ctas", "threads", "runs")}
