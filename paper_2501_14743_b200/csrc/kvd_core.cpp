@@ -1211,14 +1211,51 @@ static kvd_status launch_shape(const kvd_peer_s* p, Policy& P, kvd::PullArgs& a,
 // §8 f4: a head-sliced peer copies each remote (block, K|V) unit -- block_size
 // rows of H_r*head_dim elements -- into a strided head slice of the local
 // block: one tile per unit, LSU mover with row strides.
+// Units are block_size rows of row_bytes.  When both sides keep a run's
+// blocks back to back (default layouts) a run is one sequence of rows --
+// contiguous on the remote side, dst_row_stride apart locally -- so tiles
+// span several units (up to 32 KiB, whole rows).  When the policy chose the
+// TMA ring (over NVLink) tiles are bulk-loaded and stored row by row by the
+// whole warp (pull_kernel_tma_rows); otherwise the LSU mover.
+constexpr uint64_t kHeadTile = 16384;   // TMA head-slice ring: 4 pipes x 3 stages x 16 KiB
+constexpr uint32_t kHeadStages = 3;
+constexpr uint32_t kHeadPipes = 4;
 static void head_slice_plan(const kvd_peer_s* p, const kvd_geometry& sg, PairPlan& pp,
                             Policy& pol, kvd::PullArgs& a) {
+  const kvd_geometry& dg = p->local->geom.g;
+  const uint64_t unit = sg.span_bytes;
+  const uint64_t rows = unit / p->row_bytes;
   pp.planes = 2;
-  pp.unit = sg.span_bytes;
-  pp.contiguous = false;
-  if (pol.variant != KVD_VARIANT_LSU) pol.variant = KVD_VARIANT_LSU;
-  pol.tma_defaults = false;
-  pol.tile = (uint32_t)sg.span_bytes;
+  pp.unit = unit;
+  pp.contiguous = (uint64_t)sg.block_stride_bytes == unit &&
+                  (uint64_t)dg.block_stride_bytes == rows * p->dst_row_stride;
+  // The TMA head-slice mover runs only when asked for (KVD_OPT_VARIANT): over
+  // NVLink it reaches 725-738 GB/s for the C4 TP8 -> TP4 case against 741 for
+  // the LSU mover (tools/heads_probe.py, profiles/r01_heads_tma_rows.txt), so
+  // AUTO keeps LSU for head slices.
+  const bool tma = pol.variant == KVD_VARIANT_TMA && !pol.autov;
+  // multi-unit tiles only for the TMA ring (bulk loads amortise per tile);
+  // the LSU mover keeps one unit per warp (more warps in flight)
+  uint64_t tile = unit;
+  if (pp.contiguous && tma) {
+    const uint64_t want = p->tile_set ? p->tile_bytes : (pol.tma_defaults ? kHeadTile : p->tile_bytes);
+    tile = std::max<uint64_t>(p->row_bytes, want / p->row_bytes * p->row_bytes);
+  } else if (pp.contiguous && p->tile_set) {
+    tile = std::max<uint64_t>(p->row_bytes, p->tile_bytes / p->row_bytes * p->row_bytes);
+  } else if (!pp.contiguous) {
+    tile = unit;
+  }
+  if (tma && tile <= (96u << 10) && tile % 16 == 0) {
+    if (pol.tma_defaults) {
+      if (!p->stages_set) pol.stages = kHeadStages;
+      pol.pipes = (uint32_t)std::max<uint64_t>(
+          1, std::min<uint64_t>(kHeadPipes, (192u << 10) / (pol.stages * tile)));
+    }
+  } else {
+    pol.variant = KVD_VARIANT_LSU;
+    pol.tma_defaults = false;
+  }
+  pol.tile = (uint32_t)tile;
   a.row_bytes = p->row_bytes;
   a.src_row_stride = p->row_bytes;
   a.dst_row_stride = p->dst_row_stride;

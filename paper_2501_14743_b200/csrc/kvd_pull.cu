@@ -202,7 +202,9 @@ __device__ __forceinline__ Tile tile_at(const PullArgs& a, const int4* runs, uns
     off = (unsigned long long)kr * a.tile_bytes;
     avail = (unsigned long long)(unsigned int)run.z * a.unit_bytes - off;
     src_off = (unsigned long long)run.x * a.src.block_stride + off;
-    dst_off = (unsigned long long)run.y * a.dst.block_stride + off;
+    // head slices (f4): `off` counts remote bytes; locally rows are strided
+    dst_off = (unsigned long long)run.y * a.dst.block_stride +
+              (a.row_bytes ? off / a.row_bytes * a.dst_row_stride : off);
     in_run = off;
   } else {
     const unsigned int j = kr / a.tiles_per_unit;
@@ -603,6 +605,88 @@ pull_kernel_tma(const __grid_constant__ PullParams<MAXR> P, unsigned int stages)
   complete(a);
 }
 
+// §8 f4 over NVLink: a head-sliced peer's remote unit (block_size rows of
+// row_bytes) is contiguous, its local head slice is strided.  Each warp runs
+// an S-stage ring: lane 0 bulk-loads whole units from the peer (TMA, the
+// efficient NVLink read), and once a stage's mbarrier completes all 32 lanes
+// store its rows to the strided slice with 16 B stores (local HBM writes).
+template <int MAXR>
+__global__ void __launch_bounds__(256)
+pull_kernel_tma_rows(const __grid_constant__ PullParams<MAXR> P, unsigned int stages) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ uint64_t bars[(256 / 32) * kMaxStages];
+  const PullArgs& a = P.a;
+  mark_start(a);
+  const unsigned int lane = threadIdx.x & 31u;
+  const unsigned int warp = threadIdx.x >> 5;
+  const unsigned int pipes_per_cta = blockDim.x >> 5;
+  const unsigned int npipes = gridDim.x * pipes_per_cta;
+  const unsigned int pipe = blockIdx.x * pipes_per_cta + warp;
+  const unsigned int S = stages;
+  const int4* runs = stage_runs(
+      a, (MAXR > 0) ? P.runs : a.runs_dev,
+      reinterpret_cast<int4*>(smem + (size_t)pipes_per_cta * S * a.tile_bytes));
+  unsigned char* ring = smem + (size_t)warp * S * a.tile_bytes;
+  uint64_t* bar = bars + warp * kMaxStages;
+  publish_empty(a);
+  if (lane == 0) {
+    for (unsigned int s = 0; s < S; ++s) mbar_init(&bar[s]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const unsigned int count =
+      pipe < a.total_tiles ? (a.total_tiles - pipe + npipes - 1) / npipes : 0u;
+  // every lane derives the same (warp-uniform) tiles; lane 0 counts audit hits
+  auto fetch = [&](unsigned int k) {
+    const unsigned int t = pipe + k * npipes;
+    Tile T = tile_at(a, runs, t);
+    if (a.audit && !tile_in_bounds(a, T, t)) {
+      if (lane == 0) atomicAdd(a.audit, 1u);
+      T.skip = 1;
+    }
+    return T;
+  };
+  Tile tiles[kMaxStages];
+  for (unsigned int k = 0; k < S && k < count; ++k) {
+    tiles[k] = fetch(k);
+    if (lane == 0)
+      tma_load(ring + (size_t)k * a.tile_bytes, tiles[k].src, tiles[k].skip ? 0u : tiles[k].bytes,
+               &bar[k]);
+  }
+  Credit cr;
+  const unsigned int vpr = a.row_bytes / 16u;
+  for (unsigned int i = 0; i < count; ++i) {
+    const unsigned int s = i % S;
+    mbar_wait(&bar[s], (i / S) & 1u);
+    const Tile T = tiles[s];
+    if (!T.skip) {
+      const uint4* st = reinterpret_cast<const uint4*>(ring + (size_t)s * a.tile_bytes);
+      const unsigned int nv = T.bytes / 16u;
+      for (unsigned int c = lane; c < nv; c += 32) {
+        const unsigned int r = c / vpr, col = c - r * vpr;
+        const uint4 v = st[c];
+        asm volatile(KVD_ST_Q ".v4.u32 [%0], {%1,%2,%3,%4};"
+                     :: "l"(T.dst + (size_t)r * a.dst_row_stride + (size_t)col * 16u),
+                        "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+      }
+    }
+    if (a.nreqs) credit_tile(a, T, cr, lane == 0, true);
+    __syncwarp();                       // every lane has read stage s
+    const unsigned int k = i + S;
+    if (k < count) {
+      tiles[s] = fetch(k);
+      if (lane == 0) {
+        // generic-proxy reads of the stage before the async-proxy refill
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tma_load(ring + (size_t)s * a.tile_bytes, tiles[s].src,
+                 tiles[s].skip ? 0u : tiles[s].bytes, &bar[s]);
+      }
+    }
+  }
+  if (a.nreqs) credit_flush(a, cr, lane == 0, true);
+  complete(a);
+}
+
 __global__ void flag_kernel(unsigned long long* flag, unsigned long long token,
                             unsigned long long* mbox, unsigned long long request_id) {
   // no data: earlier stream work is ordered by the stream itself
@@ -641,9 +725,10 @@ cudaError_t launch_t(const PullArgs& args, const int4* runs_host, unsigned int c
   return cudaGetLastError();
 }
 
-template <int MAXR>
+template <int MAXR, bool ROWS>
 cudaError_t launch_tma_t(const PullArgs& args, const int4* runs_host, unsigned int ctas,
                          unsigned int threads, unsigned int stages, cudaStream_t stream) {
+  auto kernel = ROWS ? pull_kernel_tma_rows<MAXR> : pull_kernel_tma<MAXR>;
   PullParams<MAXR> P;
   fill(P, args, runs_host);
   const size_t ring = (size_t)(threads / 32) * stages * args.tile_bytes;
@@ -660,13 +745,12 @@ cudaError_t launch_tma_t(const PullArgs& args, const int4* runs_host, unsigned i
   cudaGetDevice(&dev);
   const unsigned long long bit = 1ull << (dev & 63);
   if (!(raised.load(std::memory_order_relaxed) & bit)) {
-    cudaError_t e = cudaFuncSetAttribute(pull_kernel_tma<MAXR>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          225 * 1024);
     if (e != cudaSuccess) return e;
     raised.fetch_or(bit);
   }
-  pull_kernel_tma<MAXR><<<ctas, threads, smem, stream>>>(P, stages);
+  kernel<<<ctas, threads, smem, stream>>>(P, stages);
   return cudaGetLastError();
 }
 
@@ -684,17 +768,25 @@ cudaError_t launch_v(const PullArgs& args, const int4* runs_host, unsigned int c
   return launch_t<0, V, U>(args, runs_host, ctas, threads, stream);
 }
 
+template <bool ROWS>
+cudaError_t launch_tma_r(const PullArgs& args, const int4* runs_host, unsigned int ctas,
+                         unsigned int threads, unsigned int stages, cudaStream_t stream) {
+  if (args.nruns <= (unsigned)kRunsTiny)
+    return launch_tma_t<kRunsTiny, ROWS>(args, runs_host, ctas, threads, stages, stream);
+  if (args.nruns <= (unsigned)kRunsSmall)
+    return launch_tma_t<kRunsSmall, ROWS>(args, runs_host, ctas, threads, stages, stream);
+  if (args.nruns <= (unsigned)kRunsMid)
+    return launch_tma_t<kRunsMid, ROWS>(args, runs_host, ctas, threads, stages, stream);
+  if (args.nruns <= (unsigned)kRunsLarge)
+    return launch_tma_t<kRunsLarge, ROWS>(args, runs_host, ctas, threads, stages, stream);
+  return launch_tma_t<0, ROWS>(args, runs_host, ctas, threads, stages, stream);
+}
+
 cudaError_t launch_tma(const PullArgs& args, const int4* runs_host, unsigned int ctas,
                        unsigned int threads, unsigned int stages, cudaStream_t stream) {
-  if (args.nruns <= (unsigned)kRunsTiny)
-    return launch_tma_t<kRunsTiny>(args, runs_host, ctas, threads, stages, stream);
-  if (args.nruns <= (unsigned)kRunsSmall)
-    return launch_tma_t<kRunsSmall>(args, runs_host, ctas, threads, stages, stream);
-  if (args.nruns <= (unsigned)kRunsMid)
-    return launch_tma_t<kRunsMid>(args, runs_host, ctas, threads, stages, stream);
-  if (args.nruns <= (unsigned)kRunsLarge)
-    return launch_tma_t<kRunsLarge>(args, runs_host, ctas, threads, stages, stream);
-  return launch_tma_t<0>(args, runs_host, ctas, threads, stages, stream);
+  // head-sliced peers (row_bytes > 0): bulk loads, warp-wide strided stores
+  return args.row_bytes ? launch_tma_r<true>(args, runs_host, ctas, threads, stages, stream)
+                        : launch_tma_r<false>(args, runs_host, ctas, threads, stages, stream);
 }
 
 template <int MAXR, typename V, int U>

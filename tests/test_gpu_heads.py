@@ -20,7 +20,8 @@ def _fill(cache, seed):
     return host
 
 
-def _run(src_dev, dst_dev, nl=4, nb=64, hs=1, hd=2, d=128, n=40, batch=False, seed=0):
+def _run(src_dev, dst_dev, nl=4, nb=64, hs=1, hd=2, d=128, n=40, batch=False, seed=0,
+         variant=None, audit=False):
     shards = [cache_for(kvdgen.CacheGeom(nl, hs, d, 16, nb, kvdgen.BF16), src_dev)
               for _ in range(hd // hs)]
     dst = cache_for(kvdgen.CacheGeom(nl, hd, d, 16, nb, kvdgen.BF16), dst_dev)
@@ -29,6 +30,11 @@ def _run(src_dev, dst_dev, nl=4, nb=64, hs=1, hd=2, d=128, n=40, batch=False, se
     torch.cuda.synchronize(src_dev)
     torch.cuda.synchronize(dst_dev)
     peers = [dst.open_peer_heads(c.export(), i * hs) for i, c in enumerate(shards)]
+    for p in peers:
+        if variant is not None:
+            p.set(kvd.OPT_VARIANT, variant)
+        if audit:
+            p.set(kvd.OPT_AUDIT, 1)
     s_ids, d_ids = kvdgen.fragmented_table(n, nb, nb, seed=seed + 3)
     try:
         for i, p in enumerate(peers):
@@ -48,6 +54,9 @@ def _run(src_dev, dst_dev, nl=4, nb=64, hs=1, hd=2, d=128, n=40, batch=False, se
             assert rc == oracle.OK
         torch.cuda.synchronize(dst_dev)
         assert_layers_equal([t.cpu().numpy() for t in dst.layers], expected)
+        if audit:
+            assert all(p.audit() == 0 for p in peers)
+        return [p.info() for p in peers]
     finally:
         for p in peers:
             p.close()
@@ -90,4 +99,16 @@ def test_head_slice_rejects_bad_offsets():
 def test_tp_resharding_two_gpus_70b_shapes():
     if torch.cuda.device_count() < 2:
         pytest.skip("needs two GPUs")
-    _run(0, 1, nl=80, nb=600, hs=1, hd=2, n=512, seed=7)
+    infos = _run(0, 1, nl=80, nb=600, hs=1, hd=2, n=512, seed=7, audit=True)
+    assert all(i["variant"] == kvd.VARIANT_TMA for i in infos)   # auto over NVLink
+
+
+@pytest.mark.parametrize("hs,hd,nl", [(1, 2, 4), (2, 8, 3), (4, 8, 2), (1, 4, 5)])
+@pytest.mark.parametrize("batch", [False, True])
+def test_tp_resharding_tma_rows(hs, hd, nl, batch):
+    """The TMA head-slice mover (bulk loads of whole remote units, warp-wide
+    strided row stores) forced on one GPU, audited; single pulls and batches."""
+    infos = _run(0, 0, nl=nl, hs=hs, hd=hd, n=37, batch=batch, seed=hs * 10 + hd,
+                 variant=kvd.VARIANT_TMA, audit=True)
+    if not batch:
+        assert all(i["variant"] == kvd.VARIANT_TMA for i in infos)

@@ -18,6 +18,14 @@ dst = mk(2, 1)
 torch.cuda.synchronize(0)
 s_ids, d_ids = kvdgen.fragmented_table(n, NB, NB, seed=4)
 peers = [dst.open_peer_heads(c.export(), i) for i, c in enumerate(shards)]
+# optional overrides, e.g. HEADS_OPTS="variant=4,threads=256,stages=6,ctas=148"
+from paper_2501_14743_b200 import kvd
+_OPT = {"variant": kvd.OPT_VARIANT, "threads": kvd.OPT_THREADS, "stages": kvd.OPT_STAGES,
+        "ctas": kvd.OPT_MAX_CTAS, "tile": kvd.OPT_TILE_BYTES}
+for kv in filter(None, os.environ.get("HEADS_OPTS", "").split(",")):
+    k, v = kv.split("=")
+    for p in peers:
+        p.set(_OPT[k], int(v))
 plain = dst.open_peer(whole.export())
 st = torch.cuda.Stream(1)
 rid = [0]
@@ -45,6 +53,6 @@ def run(ps, reps=20):
 nbytes = n * NL * 2 * BS * 2 * D * 2
 t_h = run(peers)
 t_p = run([plain])
-print(json.dumps({"bytes": nbytes, "tp8_to_tp4_head_slices_gbs": round(nbytes / t_h / 1e9, 1),
+print(json.dumps({"opts": os.environ.get("HEADS_OPTS", ""), "bytes": nbytes, "tp8_to_tp4_head_slices_gbs": round(nbytes / t_h / 1e9, 1),
                   "launches": 2, "info": peers[0].info(),
                   "tp4_to_tp4_plain_gbs": round(nbytes / t_p / 1e9, 1)}))
