@@ -100,7 +100,10 @@ def test_tp_resharding_two_gpus_70b_shapes():
     if torch.cuda.device_count() < 2:
         pytest.skip("needs two GPUs")
     infos = _run(0, 1, nl=80, nb=600, hs=1, hd=2, n=512, seed=7, audit=True)
-    assert all(i["variant"] == kvd.VARIANT_TMA for i in infos)   # auto over NVLink
+    assert all(i["variant"] == kvd.VARIANT_LSU for i in infos)   # AUTO: LSU for head slices
+    infos = _run(0, 1, nl=80, nb=600, hs=1, hd=2, n=512, seed=8, audit=True,
+                 variant=kvd.VARIANT_TMA)                        # the TMA head mover over NVLink
+    assert all(i["variant"] == kvd.VARIANT_TMA for i in infos)
 
 
 @pytest.mark.parametrize("hs,hd,nl", [(1, 2, 4), (2, 8, 3), (4, 8, 2), (1, 4, 5)])
