@@ -672,6 +672,23 @@ kvd_status kvd_blob_info(const void* blob, size_t blob_len, kvd_layout* layout, 
   return KVD_OK;
 }
 
+}  // extern "C"
+
+// Frees everything a cache owns (also on kvd_register_cache's error paths).
+static void cache_release(kvd_cache c) {
+  if (!c) return;
+  if (c->device >= 0) {
+    DeviceGuard dg(c->device);
+    if (c->d_bases) cudaFree(c->d_bases);
+    if (c->mbox_dev) cudaFree(c->mbox_dev);
+    if (c->mbox_stream) cudaStreamDestroy(c->mbox_stream);
+    if (c->mbox_pinned) cudaFreeHost(c->mbox_pinned);
+  }
+  delete c;
+}
+
+extern "C" {
+
 // ===========================================================================
 // ABI: a1 register
 // ===========================================================================
@@ -702,7 +719,8 @@ kvd_status kvd_register_cache(int device, const kvd_layout* layout, void* const*
                     (unsigned long long)g.g.layer_bytes);
     }
   }
-  std::unique_ptr<kvd_cache_s> c(new (std::nothrow) kvd_cache_s());
+  std::unique_ptr<kvd_cache_s, void (*)(kvd_cache)> c(new (std::nothrow) kvd_cache_s(),
+                                                     cache_release);
   if (!c) return fail(KVD_ENOMEM, "host allocation");
   c->device = device;
   c->geom = g;
@@ -716,14 +734,7 @@ kvd_status kvd_register_cache(int device, const kvd_layout* layout, void* const*
 
 kvd_status kvd_unregister_cache(kvd_cache c) {
   if (!c) return fail(KVD_EINVAL, "null cache");
-  {
-    DeviceGuard dg(c->device);
-    if (c->d_bases) cudaFree(c->d_bases);
-    if (c->mbox_dev) cudaFree(c->mbox_dev);
-    if (c->mbox_stream) cudaStreamDestroy(c->mbox_stream);
-    if (c->mbox_pinned) cudaFreeHost(c->mbox_pinned);
-  }
-  delete c;
+  cache_release(c);
   return KVD_OK;
 }
 
