@@ -23,6 +23,7 @@
 #include <memory>
 #include <mutex>
 #include <random>
+#include <thread>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -1639,11 +1640,12 @@ kvd_status kvd_poll_done(kvd_peer p, uint64_t request_id, int* done) {
 
 kvd_status kvd_wait_done(kvd_peer p, uint64_t request_id, int64_t timeout_us) {
   const auto t0 = std::chrono::steady_clock::now();
-  for (;;) {
+  for (uint64_t spin = 1;; ++spin) {
     int done = 0;
     kvd_status s = kvd_poll_done(p, request_id, &done);
     if (s != KVD_OK) return s;
     if (done) return KVD_OK;
+    if ((spin & 255u) == 0) std::this_thread::yield();   // long waits: let other threads run
     if (timeout_us >= 0 &&
         std::chrono::duration_cast<std::chrono::microseconds>(std::chrono::steady_clock::now() - t0)
                 .count() > timeout_us)
