@@ -514,6 +514,7 @@ struct kvd_peer_s {
   bool closed = false;
   unsigned int* audit_ctr = nullptr;        // KVD_OPT_AUDIT violation counter (device)
   bool timing = false;                      // KVD_OPT_TIMING
+  unsigned int* tile_ctrs = nullptr;        // per-slot dynamic tile counters (device, 0 idle)
   unsigned long long* gt_start = nullptr;   // per-slot earliest CTA start (device, ~0 idle)
   unsigned long long* gt_host = nullptr;    // per-slot duration ns (pinned, host-mapped)
   unsigned long long* gt_dev = nullptr;
@@ -862,6 +863,7 @@ static void peer_release(kvd_peer p) {
   if (p->audit_ctr) cudaFree(p->audit_ctr);
   if (p->gt_start) cudaFree(p->gt_start);
   if (p->gt_host) cudaFreeHost(p->gt_host);
+  if (p->tile_ctrs) cudaFree(p->tile_ctrs);
   for (auto s : p->streams) cudaStreamDestroy(s);
   for (auto e : p->join_events) cudaEventDestroy(e);
   if (p->fork_event) cudaEventDestroy(p->fork_event);
@@ -999,6 +1001,8 @@ static kvd_status open_impl(kvd_cache local, const void* blob, size_t blob_len,
   KVD_CUDA(cudaMemset(p->counters, 0, kSlots * sizeof(unsigned int)));
   KVD_CUDA(cudaMalloc(&p->bytectr, kSlots * sizeof(unsigned long long)));
   KVD_CUDA(cudaMemset(p->bytectr, 0, kSlots * sizeof(unsigned long long)));
+  KVD_CUDA(cudaMalloc(&p->tile_ctrs, kSlots * sizeof(unsigned int)));
+  KVD_CUDA(cudaMemset(p->tile_ctrs, 0, kSlots * sizeof(unsigned int)));
   KVD_CUDA(cudaMalloc(&p->gt_start, kSlots * sizeof(unsigned long long)));
   KVD_CUDA(cudaMemset(p->gt_start, 0xff, kSlots * sizeof(unsigned long long)));
   KVD_CUDA(cudaHostAlloc((void**)&p->gt_host, kSlots * sizeof(unsigned long long),
@@ -1429,6 +1433,9 @@ static kvd_status transfer(kvd_peer p, uint64_t request_id, const int32_t* src_i
     uint32_t threads = 0, ctas = 0;
     s = launch_shape(p, pol, a, info.bytes, &threads, &ctas);
     if (s != KVD_OK) return s;
+#ifndef KVD_EXPERIMENT_STATIC_TILES
+    if (variant == KVD_VARIANT_TMA && !p->row_bytes) a.tile_ctr = p->tile_ctrs + slot;
+#endif
     timing_begin(p, stream);
     e = kvd::launch_pull(a, p->runs4.data(), variant, ctas, threads, pol.stages, stream);
     timing_end(p, stream);

@@ -64,6 +64,10 @@ struct PullArgs {
   // host-mapped) before it releases the slot word.  nullptr: off.
   unsigned long long* gt_start;
   unsigned long long* gt_out;
+  // TMA single pulls: per-slot tile counter (device, zero at launch) from
+  // which pipes claim tiles dynamically; reset by the last CTA.  nullptr:
+  // static grid-stride order.
+  unsigned int* tile_ctr;
 
   // TP-resharding (§8 f4): row_bytes > 0 makes every unit block_size rows
   // of row_bytes, src_row_stride / dst_row_stride apart, and shifts the

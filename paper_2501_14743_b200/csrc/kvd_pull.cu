@@ -405,6 +405,7 @@ __device__ __forceinline__ void complete(const PullArgs& a) {
     if (prev == gridDim.x - 1) {
       *a.counter = 0u;
       fence_acq_rel_gpu();
+      if (a.tile_ctr != nullptr) *a.tile_ctr = 0u;   // every claim happened before its CTA arrived
       if (a.gt_start != nullptr) {   // first CTA start -> last CTA done, before the release
         const unsigned long long t1 = globaltimer();
         *(volatile unsigned long long*)a.gt_out = t1 - *(volatile unsigned long long*)a.gt_start;
@@ -560,6 +561,22 @@ pull_kernel_tma(const __grid_constant__ PullParams<MAXR> P, unsigned int stages)
     if (my_groups && pipe + (my_groups - 1) * npipes == groups - 1)
       count -= groups * K - a.total_tiles;   // this pipe owns the partial last group
     auto tile_of = [&](unsigned int i) { return ((i / K) * npipes + pipe) * K + i % K; };
+    // Single requests with a tile counter (a.tile_ctr) hand tiles out
+    // dynamically instead: a pipe claims kClaim consecutive tiles at a time,
+    // so the pipes finish within a few tiles of each other (no static
+    // imbalance at the tail) and the front still sweeps the request in order.
+    constexpr unsigned int kNone = 0xffffffffu, kClaim = 4;
+    unsigned int handed = 0, cur = 0, cur_end = 0;
+    auto next = [&]() -> unsigned int {
+      if (a.tile_ctr == nullptr) return handed < count ? tile_of(handed++) : kNone;
+      if (cur == cur_end) {
+        const unsigned int base = atomicAdd(a.tile_ctr, kClaim);
+        if (base >= a.total_tiles) return kNone;
+        cur = base;
+        cur_end = min(base + kClaim, a.total_tiles);
+      }
+      return cur++;
+    };
     Tile tiles[kMaxStages];
     // batched drain: a tile is credited to its request(s) only once its bulk
     // store has COMPLETED; credits lag the stores by kCreditLag groups so the
@@ -567,12 +584,16 @@ pull_kernel_tma(const __grid_constant__ PullParams<MAXR> P, unsigned int stages)
     constexpr unsigned int kCreditLag = 4;
     Tile pend[kCreditLag + 1];
     Credit cr;
-    for (unsigned int k = 0; k < S && k < count; ++k) {
-      tiles[k] = audited(a, tile_at(a, runs, tile_of(k)), tile_of(k));
+    unsigned int issued = 0;                 // tiles loaded into the ring so far
+    for (unsigned int k = 0; k < S; ++k) {
+      const unsigned int t = next();
+      if (t == kNone) break;
+      tiles[k] = audited(a, tile_at(a, runs, t), t);
       tma_load(ring + (size_t)k * a.tile_bytes, tiles[k].src, tiles[k].skip ? 0u : tiles[k].bytes,
                &bar[k]);
+      ++issued;
     }
-    for (unsigned int i = 0; i < count; ++i) {
+    for (unsigned int i = 0; i < issued; ++i) {
       const unsigned int s = i % S;
       mbar_wait(&bar[s], (i / S) & 1u);
       tma_store(tiles[s].dst, ring + (size_t)s * a.tile_bytes, tiles[s].skip ? 0u : tiles[s].bytes);
@@ -580,12 +601,16 @@ pull_kernel_tma(const __grid_constant__ PullParams<MAXR> P, unsigned int stages)
       if (i >= 1) {
         const unsigned int sp = (i - 1) % S;
         tma_wait_read_1();   // store i-1 has finished reading its stage
-        // refill the stage of tile i-1 with tile i-1+S
-        const unsigned int k = i - 1 + S;
-        if (k < count) {
-          tiles[sp] = audited(a, tile_at(a, runs, tile_of(k)), tile_of(k));
-          tma_load(ring + (size_t)sp * a.tile_bytes, tiles[sp].src,
-                   tiles[sp].skip ? 0u : tiles[sp].bytes, &bar[sp]);
+        // refill the stage of tile i-1 with the ring's tile number i-1+S
+        // (only while no claim has failed: tile j always lives in stage j % S)
+        if (issued == i - 1 + S) {
+          const unsigned int t = next();
+          if (t != kNone) {
+            tiles[sp] = audited(a, tile_at(a, runs, t), t);
+            tma_load(ring + (size_t)sp * a.tile_bytes, tiles[sp].src,
+                     tiles[sp].skip ? 0u : tiles[sp].bytes, &bar[sp]);
+            ++issued;
+          }
         }
       }
       if (a.nreqs && i >= kCreditLag) {
@@ -595,8 +620,8 @@ pull_kernel_tma(const __grid_constant__ PullParams<MAXR> P, unsigned int stages)
     }
     tma_wait_all();
     if (a.nreqs) {
-      const unsigned int first = count > kCreditLag ? count - kCreditLag : 0u;
-      for (unsigned int j = first; j < count; ++j)
+      const unsigned int first = issued > kCreditLag ? issued - kCreditLag : 0u;
+      for (unsigned int j = first; j < issued; ++j)
         credit_tile(a, pend[j % (kCreditLag + 1)], cr, true, false);
       credit_flush(a, cr, true, false);
     }
