@@ -101,6 +101,20 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+// Programmatic dependent launch: pull kernels are launched with
+// programmatic stream serialisation, so a pull queued right behind another
+// pull can be scheduled while the first one drains.  Each CTA lets its
+// dependents launch once it has finished moving its share (pdl_trigger), and
+// every pull waits for the preceding grid to complete and flush before it
+// touches any global memory (pdl_wait) -- stream order is unchanged, only the
+// launch latency overlaps the tail.  After a non-PDL kernel both are no-ops.
+__device__ __forceinline__ void pdl_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // KVD_OPT_TIMING: the earliest CTA start of this launch (see PullArgs::gt_start)
 __device__ __forceinline__ void mark_start(const PullArgs& a) {
   if (a.gt_start != nullptr && threadIdx.x == 0) atomicMin(a.gt_start, globaltimer());
@@ -439,6 +453,7 @@ __global__ void __launch_bounds__(512, 2)
 pull_kernel(const __grid_constant__ PullParams<MAXR> P) {
   extern __shared__ int4 s_runs[];
   const PullArgs& a = P.a;
+  pdl_wait();
   mark_start(a);
   const int4* runs = stage_runs(a, (MAXR > 0) ? P.runs : a.runs_dev, s_runs);
   const unsigned int lane = threadIdx.x & 31u;
@@ -465,6 +480,7 @@ pull_kernel(const __grid_constant__ PullParams<MAXR> P) {
     if (GENERAL && a.nreqs) credit_tile(a, T, cr, lane == 0, true);   // batched drain
   }
   if (GENERAL && a.nreqs) credit_flush(a, cr, lane == 0, true);
+  pdl_trigger();
   complete(a);
 }
 
@@ -530,6 +546,7 @@ pull_kernel_tma(const __grid_constant__ PullParams<MAXR> P, unsigned int stages)
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint64_t bars[(256 / 32) * kMaxStages];   // <= 8 pipes (launch bound)
   const PullArgs& a = P.a;
+  pdl_wait();
   mark_start(a);
   const unsigned int warp = threadIdx.x >> 5;
   const unsigned int pipes_per_cta = blockDim.x >> 5;
@@ -627,6 +644,7 @@ pull_kernel_tma(const __grid_constant__ PullParams<MAXR> P, unsigned int stages)
     }
   }
   __syncwarp();
+  pdl_trigger();
   complete(a);
 }
 
@@ -641,6 +659,7 @@ pull_kernel_tma_rows(const __grid_constant__ PullParams<MAXR> P, unsigned int st
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint64_t bars[(256 / 32) * kMaxStages];
   const PullArgs& a = P.a;
+  pdl_wait();
   mark_start(a);
   const unsigned int lane = threadIdx.x & 31u;
   const unsigned int warp = threadIdx.x >> 5;
@@ -709,6 +728,7 @@ pull_kernel_tma_rows(const __grid_constant__ PullParams<MAXR> P, unsigned int st
     }
   }
   if (a.nreqs) credit_flush(a, cr, lane == 0, true);
+  pdl_trigger();
   complete(a);
 }
 
@@ -735,6 +755,27 @@ void fill(PullParams<MAXR>& P, const PullArgs& args, const int4* runs_host) {
 constexpr unsigned int kStageMinRuns = 64;
 constexpr size_t kStageMaxBytes = 32 * 1024;
 
+// Launch with programmatic stream serialisation (see pdl_wait/pdl_trigger).
+template <typename Kernel, typename... Args>
+cudaError_t launch_pdl(Kernel kernel, unsigned int ctas, unsigned int threads, size_t smem,
+                       cudaStream_t stream, const Args&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ctas);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+#ifdef KVD_EXPERIMENT_NO_PDL
+  cfg.numAttrs = 0;
+#else
+  cfg.numAttrs = 1;
+#endif
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 template <int MAXR, typename V, int U>
 cudaError_t launch_t(const PullArgs& args, const int4* runs_host, unsigned int ctas,
                      unsigned int threads, cudaStream_t stream) {
@@ -744,10 +785,8 @@ cudaError_t launch_t(const PullArgs& args, const int4* runs_host, unsigned int c
   const bool stage = args.nruns > kStageMinRuns && table <= kStageMaxBytes;
   P.a.smem_runs = stage ? 1u : 0u;
   if (args.nreqs || args.row_bytes)
-    pull_kernel<MAXR, V, U, true><<<ctas, threads, stage ? table : 0, stream>>>(P);
-  else
-    pull_kernel<MAXR, V, U, false><<<ctas, threads, stage ? table : 0, stream>>>(P);
-  return cudaGetLastError();
+    return launch_pdl(pull_kernel<MAXR, V, U, true>, ctas, threads, stage ? table : 0, stream, P);
+  return launch_pdl(pull_kernel<MAXR, V, U, false>, ctas, threads, stage ? table : 0, stream, P);
 }
 
 template <int MAXR, bool ROWS>
@@ -775,8 +814,7 @@ cudaError_t launch_tma_t(const PullArgs& args, const int4* runs_host, unsigned i
     if (e != cudaSuccess) return e;
     raised.fetch_or(bit);
   }
-  kernel<<<ctas, threads, smem, stream>>>(P, stages);
-  return cudaGetLastError();
+  return launch_pdl(kernel, ctas, threads, smem, stream, P, stages);
 }
 
 template <typename V, int U>

@@ -53,6 +53,8 @@ def main():
     ap.add_argument("--stages", type=int, default=0)
     ap.add_argument("--ctas", type=int, default=0)
     ap.add_argument("--modes", default="single,batch,merged")
+    ap.add_argument("--no-timing", action="store_true",
+                    help="no KVD_OPT_TIMING events between launches (they break PDL adjacency)")
     ap.add_argument("--ipc", action="store_true",
                     help="prefill cache in a second process (CUDA IPC mapping, as deployed)")
     a = ap.parse_args()
@@ -90,7 +92,8 @@ def main():
         peer.set(kvd.OPT_STAGES, a.stages)
     if a.ctas:
         peer.set(kvd.OPT_MAX_CTAS, a.ctas)
-    peer.set(kvd.OPT_TIMING, 1)   # in-kernel %globaltimer spans of single pulls
+    if not a.no_timing:
+        peer.set(kvd.OPT_TIMING, 1)   # in-kernel %globaltimer spans of single pulls
     torch.cuda.set_device(a.dst_dev)
     stream = torch.cuda.Stream(a.dst_dev)
     stream2 = torch.cuda.Stream(a.dst_dev)
@@ -153,7 +156,8 @@ def main():
                     times.append(e0.elapsed_time(e1))
             ms = float(np.median(times))
             gt_ms, gt_n = peer.device_time()
-            peer.kernel_time()
+            if not a.no_timing:
+                peer.kernel_time()
             if gt_n:   # mean in-kernel span per request vs the per-request share of the step
                 res[mode + "_kernel_us_per_request"] = round(gt_ms / gt_n * 1e3, 2)
                 res[mode + "_step_us_per_request"] = round(
