@@ -214,3 +214,23 @@ def test_register_without_gpu_fails_cleanly(kvd):
     with pytest.raises(kvd.KvdError) as ei:
         kvd.kvd_register_cache(0, kvd.make_layout(2, 2, 64, 16, 0), [1 << 20, 1 << 21])
     assert ei.value.status == kvd.ELAYOUT
+
+
+def test_argument_errors_before_any_cuda_call(kvd):
+    """Entry points reject null / out-of-range arguments with the documented
+    status on a machine without a GPU too."""
+    import ctypes
+    lib = kvd._lib
+    assert lib.kvd_mem_free(None) == kvd.EINVAL
+    p = ctypes.c_void_p()
+    assert lib.kvd_mem_alloc(0, 1 << 20, 5, ctypes.byref(p), None, None) == kvd.EINVAL   # bad kind
+    assert lib.kvd_mem_alloc(0, 0, 0, ctypes.byref(p), None, None) == kvd.EINVAL         # zero bytes
+    assert lib.kvd_mem_alloc(0, 1 << 20, 0, None, None, None) == kvd.EINVAL              # null out
+    assert lib.kvd_stream_wait(None, None) == kvd.EINVAL
+    ms, n = ctypes.c_double(), ctypes.c_uint64()
+    assert lib.kvd_peer_device_time(None, ctypes.byref(ms), ctypes.byref(n)) == kvd.EINVAL
+    assert lib.kvd_peer_kernel_time(None, ctypes.byref(ms), ctypes.byref(n)) == kvd.EINVAL
+    assert lib.kvd_close_peer(None) == kvd.EINVAL
+    assert lib.kvd_unregister_cache(None) == kvd.EINVAL
+    assert lib.kvd_peer_set(None, kvd.OPT_STREAMS, 2) == kvd.EINVAL
+    assert "invalid argument" in kvd.kvd_strerror(kvd.EINVAL)
