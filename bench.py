@@ -477,6 +477,16 @@ def run_kvd(args, rank, world, local_rank):
                         lat_out.append(time.perf_counter_ns() - t0)
 
     def step(lat_out=None):
+        if lat_out is not None and n_req == 1 and not args.batch:
+            # one request: issue -> completion observed by kvd_wait_done's C-side
+            # spin on the slot word (no Python polling granularity in the number)
+            s, d = reqs[0]
+            rid[0] += 1
+            t0 = time.perf_counter_ns()
+            peer.pull(rid[0], s, d, stream)
+            peer.wait(rid[0])
+            lat_out.append(time.perf_counter_ns() - t0)
+            return
         issue()
         retire(0, lat_out)
 
