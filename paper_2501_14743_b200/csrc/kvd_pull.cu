@@ -19,8 +19,13 @@
 //             complete_tx), then shared memory -> local HBM (bulk group).
 //             Up to ~200 KiB per SM in flight without registers, so far
 //             fewer SMs saturate NVLink and the rest stay free for decode.
-// Both are bit copies through integer registers / shared memory only (no
+//             Single pulls hand tiles out dynamically (per-slot counter);
+//             head-sliced peers (§8 f4) have a variant whose stores are
+//             warp-wide strided rows (pull_kernel_tma_rows).
+// All are bit copies through integer registers / shared memory only (no
 // float type ever touches the data): NaN payloads, -0, subnormals survive.
+// Pull kernels are launched with programmatic stream serialisation
+// (griddepcontrol): back-to-back pulls overlap launch with the previous tail.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
