@@ -7,7 +7,9 @@
 //   a3  block-table validation and run coalescing
 //   a4  descriptor staging and the single launch
 //   a6  completion slots and kvd_poll_done
-// The kernel itself (a5) lives in kvd_pull.cu.
+//   f1  kvd_pull_batch; f2 kvd_push; f4 kvd_open_peer_heads
+//   f3 groundwork: VMM (POSIX-fd / fabric) exports, kvd_vmm.cpp
+// The kernels (a5) live in kvd_pull.cu.
 #include "../../include/kvd.h"
 
 #include <cuda_runtime.h>
