@@ -441,3 +441,20 @@ def test_tma_two_gpus_c4_shard():
         assert_layers_equal(pair.download_dst(), pair.expected(src, dst))
     finally:
         pair.close()
+
+
+@pytest.mark.gpu2
+@pytest.mark.parametrize("src_dev,dst_dev", [(3, 0), (2, 1), (1, 3)])
+def test_any_pair_over_nvswitch(src_dev, dst_dev):
+    """NVSwitch is uniform: any prefill GPU -> any decode GPU (SURVEY §8 d,
+    C2 "also any i -> j"), auto mover, bit-exact."""
+    if max(src_dev, dst_dev) >= torch.cuda.device_count():
+        pytest.skip("needs four GPUs")
+    g = C1.with_blocks(256)
+    pair = make_pair(g, g, seed=40 + src_dev * 4 + dst_dev, src_dev=src_dev, dst_dev=dst_dev)
+    try:
+        s, d = kvdgen.fragmented_table(120, 256, 256, seed=src_dev * 4 + dst_dev)
+        pull_and_wait(pair, s, d)
+        assert_layers_equal(pair.download_dst(), pair.expected(s, d))
+    finally:
+        pair.close()
