@@ -458,3 +458,34 @@ def test_any_pair_over_nvswitch(src_dev, dst_dev):
         assert_layers_equal(pair.download_dst(), pair.expected(s, d))
     finally:
         pair.close()
+
+
+@pytest.mark.parametrize("variant", [kvd.VARIANT_AUTO, kvd.VARIANT_TMA, kvd.VARIANT_LSU32])
+def test_back_to_back_pulls_keep_stream_order(variant):
+    """Pulls are launched with programmatic dependent launch; a second pull
+    into the SAME destination blocks right behind the first (write after
+    write) must still land after it, and a torch kernel zeroing the
+    destination before them must land before both."""
+    g = C1.with_blocks(512)
+    pair = make_pair(g, g, seed=41)
+    try:
+        pair.peer.set(kvd.OPT_VARIANT, variant)
+        rng = np.random.default_rng(3)
+        d = rng.choice(512, size=200, replace=False).astype(np.int32)
+        s1 = rng.choice(512, size=200, replace=False).astype(np.int32)
+        s2 = rng.choice(512, size=200, replace=False).astype(np.int32)
+        st = torch.cuda.Stream()
+        for _ in range(5):
+            with torch.cuda.stream(st):
+                for t in pair.dst.layers:
+                    t.zero_()
+            r1, r2 = next_request_id(), next_request_id()
+            pair.peer.pull(r1, s1, d, st)
+            pair.peer.pull(r2, s2, d, st)
+            pair.peer.wait(r1)
+            pair.peer.wait(r2)
+            st.synchronize()
+            zero = [np.zeros_like(h) for h in pair.dst_host]
+            assert_layers_equal(pair.download_dst(), pair.expected(s2, d, zero))
+    finally:
+        pair.close()
