@@ -114,7 +114,9 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 // touches any global memory (pdl_wait) -- stream order is unchanged, only the
 // launch latency overlaps the tail.  After a non-PDL kernel both are no-ops.
 __device__ __forceinline__ void pdl_wait() {
+#ifndef KVD_EXPERIMENT_NO_PDL_WAIT   // A/B only: checks the ordering test can fail
   asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
 }
 __device__ __forceinline__ void pdl_trigger() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
