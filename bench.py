@@ -742,6 +742,8 @@ def run_kvd(args, rank, world, local_rank):
             out["nccl_baseline"] = nb_out
         if not multi and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_oracle_sample()
+        else:   # the contract times the oracle on rank 0 at N = 1 only
+            out["cpu_baseline"] = None
         print(json.dumps(out), flush=True)
 
     if peer:
