@@ -24,9 +24,13 @@ arrives) and completions retired as they land.
 `value` = bytes pulled by all pairs / device time of the K steps (CUDA events
 on the pull stream, max over ranks); `e2e` = the same bytes / host wall time
 from the first kvd_pull entry to the last completion observed;
-`roofline.achieved` uses kernel-only time (library events right around each
-launch, KVD_OPT_TIMING); `p50_latency_ms` = issue -> completion observed of
-single requests on an idle pair, measured after the timed region.
+`roofline.achieved` = algorithmic bytes per launch / average launch duration,
+the latter from the CUDA events over the timed region on the pull stream
+(which holds nothing but back-to-back pull launches), cross-checked by the
+in-kernel %globaltimer span of every launch (KVD_OPT_TIMING = 2: no events
+between launches); `--timing events` instead brackets every launch with
+library events (KVD_OPT_TIMING = 1); `p50_latency_ms` = issue -> completion
+observed of single requests on an idle pair, measured after the timed region.
 """
 from __future__ import annotations
 
@@ -511,7 +515,9 @@ def run_kvd(args, rank, world, local_rank):
     sampler = ClockSampler(dev)
     launches[0] = 0
     if peer:
-        peer.set(kvd.OPT_TIMING, 1)   # library-side events right around each pull kernel
+        # timer: in-kernel %globaltimer spans only (events between launches would
+        # block programmatic dependent launch); events: library events around each launch
+        peer.set(kvd.OPT_TIMING, 1 if args.timing == "events" else 2)
     barrier()
     # Throughput: the K steps are issued back to back, as a serving engine
     # posts each request's pull when it arrives; completions are retired as
@@ -532,7 +538,8 @@ def run_kvd(args, rank, world, local_rank):
         wall = time.perf_counter() - wall0
     barrier()
     timed_launches = launches[0]
-    kern_ms_total, kern_launches = peer.kernel_time() if peer else (0.0, 0)
+    kern_ms_total, kern_launches = (peer.kernel_time() if peer and args.timing == "events"
+                                    else (0.0, 0))
     # %globaltimer cross-check (first CTA start -> last CTA done, single pulls
     # only; batches have no whole-launch arrival)
     gt_ms_total, gt_launches = peer.device_time() if peer else (0.0, 0)
@@ -611,7 +618,10 @@ def run_kvd(args, rank, world, local_rank):
     stats = {"dev_s": dev_s, "wall_s": wall if peer else 0.0,
              "bytes": bytes_per_step * K if peer else 0,
              "step_ms": float(np.mean(step_ms)) if step_ms else 0.0,
-             "kern_ms": kern_ms_total / K if peer else 0.0, "kern_launches": kern_launches,
+             # per step: launch-bracketed library events, or the timed region's own
+             # events divided by the steps (the region holds only pull launches)
+             "kern_ms": ((kern_ms_total / K if args.timing == "events" else dev_s * 1e3 / K)
+                         if peer else 0.0), "kern_launches": kern_launches,
              "gt_ms": gt_ms_total / gt_launches if gt_launches else 0.0,
              "gt_ms_total": gt_ms_total, "gt_launches": gt_launches,
              "lat": lat_ns, "clock": sampler.summary(), "info": info, "base": base,
@@ -627,9 +637,8 @@ def run_kvd(args, rank, world, local_rank):
         step_dev = max(s["step_ms"] for s in dec)
         info0 = dec[0]["info"]
         peaks, peak_src = measured_peaks()
-        # per pair: its own bytes over its own launch-bracketed step time
-        # roofline: each pair's bytes over its own kernel-only time (library
-        # events right around each launch, on the pull stream)
+        # roofline: each pair's bytes per step over its average step duration on
+        # the pull stream (see the module docstring for the two timing modes)
         per_pair = [s["bytes_per_step"] / (s["kern_ms"] / 1e3) / 1e9 for s in dec]
         kern_dev = max(s["kern_ms"] for s in dec)
         achieved_link = float(np.mean(per_pair))
@@ -773,6 +782,9 @@ def main():
     ap.add_argument("--threads", type=int, default=0)
     ap.add_argument("--max-ctas", type=int, default=0)
     ap.add_argument("--no-coalesce", action="store_true")
+    ap.add_argument("--timing", choices=["timer", "events"], default="timer",
+                    help="roofline timing: region events + in-kernel globaltimer (default) or "
+                         "library events around every launch")
     ap.add_argument("--streams", type=int, default=0,
                     help="KVD_OPT_STREAMS: >= 2 lets consecutive pulls overlap on library "
                          "streams (completion still polled per request)")

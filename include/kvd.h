@@ -142,7 +142,9 @@ typedef enum {
   KVD_OPT_TIMING = 7,       /* 1: record CUDA events right around every pull kernel on the
                                caller's stream (kvd_peer_kernel_time sums them) and have single
                                pulls measure first-CTA-start -> last-CTA-done with %globaltimer
-                               (kvd_peer_device_time).  0 (default) off */
+                               (kvd_peer_device_time).  2: the %globaltimer spans only (no events
+                               between launches, so back-to-back pulls still overlap launch and
+                               tail).  0 (default) off */
   KVD_OPT_STREAMS = 8       /* 0 or 1 (default): every transfer runs on the caller's stream, in
                                stream order.  k in [2, 8]: a transfer still waits for the work
                                already on the caller's stream, but runs on the next of k library

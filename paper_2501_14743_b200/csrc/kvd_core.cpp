@@ -515,7 +515,8 @@ struct kvd_peer_s {
   kvd_pull_info last{};
   bool closed = false;
   unsigned int* audit_ctr = nullptr;        // KVD_OPT_AUDIT violation counter (device)
-  bool timing = false;                      // KVD_OPT_TIMING
+  bool timing = false;                      // KVD_OPT_TIMING != 0: %globaltimer spans
+  bool timing_events = false;               // KVD_OPT_TIMING == 1: also CUDA events per launch
   unsigned int* tile_ctrs = nullptr;        // per-slot dynamic tile counters (device, 0 idle)
   unsigned long long* gt_start = nullptr;   // per-slot earliest CTA start (device, ~0 idle)
   unsigned long long* gt_host = nullptr;    // per-slot duration ns (pinned, host-mapped)
@@ -1075,7 +1076,9 @@ kvd_status kvd_peer_set(kvd_peer p, int option, int64_t value) {
       p->stages_set = true;
       return KVD_OK;
     case KVD_OPT_TIMING:
+      if (value < 0 || value > 2) return fail(KVD_EINVAL, "timing must be 0, 1 or 2");
       p->timing = value != 0;
+      p->timing_events = value == 1;
       return KVD_OK;
     case KVD_OPT_STREAMS: {
       if (value < 0 || value > 8) return fail(KVD_EINVAL, "streams must be in [0, 8]");
@@ -1299,7 +1302,7 @@ static cudaError_t route_stream(kvd_peer_s* p, cudaStream_t user, cudaStream_t* 
 }
 
 static void timing_begin(kvd_peer_s* p, cudaStream_t s) {
-  if (!p->timing) return;
+  if (!p->timing_events) return;
   std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
   if (!p->event_pool.empty()) {
     ev = p->event_pool.back();
@@ -1312,7 +1315,7 @@ static void timing_begin(kvd_peer_s* p, cudaStream_t s) {
   p->timed.push_back(ev);
 }
 static void timing_end(kvd_peer_s* p, cudaStream_t s) {
-  if (p->timing && !p->timed.empty()) cudaEventRecord(p->timed.back().second, s);
+  if (p->timing_events && !p->timed.empty()) cudaEventRecord(p->timed.back().second, s);
 }
 
 // Pull (push = false): remote (imported) cache -> local cache, kernel on the
@@ -1716,7 +1719,7 @@ kvd_status kvd_peer_audit(kvd_peer p, uint64_t* violations) {
 kvd_status kvd_peer_kernel_time(kvd_peer p, double* total_ms, uint64_t* launches) {
   if (!p || !total_ms || !launches) return fail(KVD_EINVAL, "null argument");
   std::lock_guard<std::mutex> lk(p->mu);
-  if (!p->timing) return fail(KVD_ESTATE, "timing is off (set KVD_OPT_TIMING)");
+  if (!p->timing_events) return fail(KVD_ESTATE, "launch events are off (set KVD_OPT_TIMING = 1)");
   DeviceGuard dg(p->local->device);
   if (!dg.ok) return fail(KVD_ECUDA, "cannot select device %d", p->local->device);
   double sum = 0;
