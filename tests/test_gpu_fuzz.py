@@ -1,6 +1,7 @@
 """Randomised parity: random geometries, layouts, block tables, movers and
 launch shapes -- every pull bit-exact against the oracle, with the in-kernel
 bounds audit on (zero violations).  Seeded, so failures reproduce."""
+import os
 import random
 
 import numpy as np
@@ -48,16 +49,23 @@ def _opts(rng):
         o[kvd.OPT_THREADS] = 32 * rng.choice([1, 2, 4])
         o[kvd.OPT_STAGES] = rng.choice([2, 3, 4])
         o[kvd.OPT_TILE_BYTES] = min(o.get(kvd.OPT_TILE_BYTES, 4096), 16384)
+        # the ring (pipes x stages x tile) must fit 225 KiB of shared memory,
+        # else kvd_pull refuses it with KVD_EINVAL (tested in test_gpu_parity)
+        while (o[kvd.OPT_THREADS] // 32) * o[kvd.OPT_STAGES] * o[kvd.OPT_TILE_BYTES] > 225 * 1024:
+            o[kvd.OPT_TILE_BYTES] //= 2
     elif rng.random() < 0.5:
         o[kvd.OPT_THREADS] = 32 * rng.choice([1, 4, 8, 16])
     if rng.random() < 0.3:
         o[kvd.OPT_MAX_CTAS] = rng.randint(1, 9)
     if rng.random() < 0.2:
         o[kvd.OPT_COALESCE] = 0
+    if rng.random() < 0.25:
+        o[kvd.OPT_STREAMS] = 2                     # library streams (completion via wait)
     return o
 
 
-@pytest.mark.parametrize("seed", range(200))
+# KVD_FUZZ_SEEDS=N widens the sweep (a 3000-seed soak ran once)
+@pytest.mark.parametrize("seed", range(int(os.environ.get("KVD_FUZZ_SEEDS", "200"))))
 def test_fuzz_pull(seed):
     rng = random.Random(seed)
     g = _geom(rng)
