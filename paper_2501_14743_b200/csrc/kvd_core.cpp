@@ -1600,6 +1600,14 @@ kvd_status kvd_pull_batch(kvd_peer p, uint32_t num_requests, const uint64_t* req
   uint32_t threads = 0, ctas = 0;
   s = launch_shape(p, pol, a, (uint64_t)n * per_entry, &threads, &ctas);
   if (s != KVD_OK) return s;
+#ifndef KVD_EXPERIMENT_STATIC_TILES
+  if (pol.variant == KVD_VARIANT_TMA && !p->row_bytes) {
+    // dynamic tile claiming; the first request's (otherwise unused) arrival
+    // counter only tells the last CTA to reset the tile counter
+    a.counter = p->counters + slots[0];
+    a.tile_ctr = p->tile_ctrs + slots[0];
+  }
+#endif
   timing_begin(p, stream);
   cudaError_t e = kvd::launch_pull(a, p->runs4.data(), pol.variant, ctas, threads, pol.stages, stream);
   timing_end(p, stream);

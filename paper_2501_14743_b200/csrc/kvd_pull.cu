@@ -427,6 +427,7 @@ __device__ __forceinline__ void complete(const PullArgs& a) {
       *a.counter = 0u;
       fence_acq_rel_gpu();
       if (a.tile_ctr != nullptr) *a.tile_ctr = 0u;   // every claim happened before its CTA arrived
+      if (a.nreqs) return;           // batches: requests completed one by one (publish)
       if (a.gt_start != nullptr) {   // first CTA start -> last CTA done, before the release
         const unsigned long long t1 = globaltimer();
         *(volatile unsigned long long*)a.gt_out = t1 - *(volatile unsigned long long*)a.gt_start;
@@ -588,11 +589,12 @@ pull_kernel_tma(const __grid_constant__ PullParams<MAXR> P, unsigned int stages)
     if (my_groups && pipe + (my_groups - 1) * npipes == groups - 1)
       count -= groups * K - a.total_tiles;   // this pipe owns the partial last group
     auto tile_of = [&](unsigned int i) { return ((i / K) * npipes + pipe) * K + i % K; };
-    // Single requests with a tile counter (a.tile_ctr) hand tiles out
-    // dynamically instead: a pipe claims kClaim consecutive tiles at a time,
+    // With a tile counter (a.tile_ctr) tiles are handed out dynamically
+    // instead: a pipe claims kClaim consecutive tiles at a time,
     // so the pipes finish within a few tiles of each other (no static
     // imbalance at the tail) and the front still sweeps the request in order.
-    constexpr unsigned int kNone = 0xffffffffu, kClaim = 4;
+    constexpr unsigned int kNone = 0xffffffffu;
+    const unsigned int kClaim = a.nreqs ? K : 4u;   // batches: claim credit-friendly groups
     unsigned int handed = 0, cur = 0, cur_end = 0;
     auto next = [&]() -> unsigned int {
       if (a.tile_ctr == nullptr) return handed < count ? tile_of(handed++) : kNone;
