@@ -355,6 +355,13 @@ KVD_API kvd_status kvd_poll_released(kvd_cache exporter, uint64_t* request_ids, 
 /* Spin on kvd_poll_done until done or `timeout_us` elapses (KVD_EBUSY). */
 KVD_API kvd_status kvd_wait_done(kvd_peer peer, uint64_t request_id, int64_t timeout_us);
 
+/* kvd_poll_done over n in-flight requests in one call (a decode loop admitting
+ * many requests): done[i] = 1 and the request retired when it completed, else
+ * 0; *ndone = how many completed.  KVD_EINVAL for a request not in flight
+ * (entries before it have been processed).  Makes no CUDA call. */
+KVD_API kvd_status kvd_poll_many(kvd_peer peer, const uint64_t* request_ids, uint32_t n,
+                                 uint8_t* done, uint32_t* ndone);
+
 /* Bounds-audit violations counted on this peer since KVD_OPT_AUDIT was set
  * (synchronises the local device first).  KVD_ESTATE if auditing is off. */
 KVD_API kvd_status kvd_peer_audit(kvd_peer peer, uint64_t* violations);

@@ -1658,6 +1658,32 @@ kvd_status kvd_poll_done(kvd_peer p, uint64_t request_id, int* done) {
   return KVD_OK;
 }
 
+kvd_status kvd_poll_many(kvd_peer p, const uint64_t* request_ids, uint32_t n, uint8_t* done,
+                         uint32_t* ndone) {
+  if (!p || !ndone || (n && (!request_ids || !done))) return fail(KVD_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lk(p->mu);
+  uint32_t k = 0;
+  for (uint32_t i = 0; i < n; ++i) {
+    done[i] = 0;
+    auto it = p->inflight.find(request_ids[i]);
+    if (it == p->inflight.end())
+      return fail(KVD_EINVAL, "request %llu is not in flight", (unsigned long long)request_ids[i]);
+    const uint32_t slot = it->second.slot;
+    if (__atomic_load_n(&p->flags[slot], __ATOMIC_ACQUIRE) != it->second.token) continue;
+    done[i] = 1;
+    ++k;
+    p->slot_seq[slot] = 0;
+    if (it->second.timed) {
+      p->gt_total_ms += (double)__atomic_load_n(&p->gt_host[slot], __ATOMIC_RELAXED) * 1e-6;
+      ++p->gt_count;
+    }
+    if (it->second.batch >= 0) --p->batch_bufs[it->second.batch].refs;
+    p->inflight.erase(it);
+  }
+  *ndone = k;
+  return KVD_OK;
+}
+
 kvd_status kvd_wait_done(kvd_peer p, uint64_t request_id, int64_t timeout_us) {
   const auto t0 = std::chrono::steady_clock::now();
   for (uint64_t spin = 1;; ++spin) {

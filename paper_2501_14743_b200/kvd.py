@@ -30,6 +30,7 @@ EXPORTED = (
     "kvd_open_peer_heads",
     "kvd_close_peer",
     "kvd_peer_set", "kvd_pull", "kvd_push", "kvd_pull_batch", "kvd_poll_done", "kvd_wait_done",
+    "kvd_poll_many",
     "kvd_last_pull_info", "kvd_peer_audit", "kvd_peer_kernel_time", "kvd_peer_device_time",
     "kvd_stream_wait",
     "kvd_poll_released",
@@ -106,6 +107,7 @@ _SIGS = {
     "kvd_pull_batch": [_p, _u32, _p, _p, _p, _p, _p],
     "kvd_poll_done": [_p, _u64, ctypes.POINTER(ctypes.c_int)],
     "kvd_wait_done": [_p, _u64, _i64],
+    "kvd_poll_many": [_p, _p, _u32, _p, ctypes.POINTER(_u32)],
     "kvd_last_pull_info": [_p, ctypes.POINTER(kvd_pull_info)],
     "kvd_peer_audit": [_p, ctypes.POINTER(_u64)],
     "kvd_poll_released": [_p, _p, _u32, ctypes.POINTER(_u32)],
@@ -313,6 +315,16 @@ def kvd_poll_done(peer: int, request_id: int) -> bool:
     done = ctypes.c_int(0)
     _check(_lib.kvd_poll_done(peer, request_id, ctypes.byref(done)), "kvd_poll_done")
     return bool(done.value)
+
+
+def kvd_poll_many(peer: int, request_ids) -> list:
+    """Retire every completed request among `request_ids`; returns those ids."""
+    ids = np.ascontiguousarray(np.asarray(request_ids, dtype=np.uint64).reshape(-1))
+    done = np.zeros(max(1, ids.size), dtype=np.uint8)
+    n = _u32(0)
+    _check(_lib.kvd_poll_many(peer, _addr(ids) if ids.size else None, ids.size, _addr(done),
+                              ctypes.byref(n)), "kvd_poll_many")
+    return [int(x) for x in ids[done[:ids.size] != 0]]
 
 
 def kvd_wait_done(peer: int, request_id: int, timeout_us: int = 10_000_000) -> None:

@@ -135,6 +135,10 @@ class Peer:
     def poll(self, request_id: int) -> bool:
         return kvd.kvd_poll_done(self.handle, request_id)
 
+    def poll_many(self, request_ids) -> list:
+        """Completed (and now retired) ids among `request_ids`, one C call."""
+        return kvd.kvd_poll_many(self.handle, request_ids)
+
     def wait(self, request_id: int, timeout_us: int = 30_000_000) -> None:
         kvd.kvd_wait_done(self.handle, request_id, timeout_us)
 

@@ -227,6 +227,8 @@ def test_argument_errors_before_any_cuda_call(kvd):
     assert lib.kvd_mem_alloc(0, 0, 0, ctypes.byref(p), None, None) == kvd.EINVAL         # zero bytes
     assert lib.kvd_mem_alloc(0, 1 << 20, 0, None, None, None) == kvd.EINVAL              # null out
     assert lib.kvd_stream_wait(None, None) == kvd.EINVAL
+    nd = ctypes.c_uint32()
+    assert lib.kvd_poll_many(None, None, 0, None, ctypes.byref(nd)) == kvd.EINVAL
     ms, n = ctypes.c_double(), ctypes.c_uint64()
     assert lib.kvd_peer_device_time(None, ctypes.byref(ms), ctypes.byref(n)) == kvd.EINVAL
     assert lib.kvd_peer_kernel_time(None, ctypes.byref(ms), ctypes.byref(n)) == kvd.EINVAL

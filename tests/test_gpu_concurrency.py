@@ -142,3 +142,32 @@ def test_library_streams_overlap_and_order():
         pair.peer.wait(rid)
     finally:
         pair.close()
+
+
+def test_poll_many_retires_completed_requests():
+    """kvd_poll_many: one call reports (and retires) every completed request."""
+    from paper_2501_14743_b200 import kvd
+    pair = make_pair(G, G, seed=74)
+    try:
+        tables = kvdgen.disjoint_fragmented_tables([30, 45, 12, 60, 7], 512, 512, seed=9)
+        rids = []
+        for s, d in tables:
+            rid = next_request_id()
+            pair.peer.pull(rid, s, d)
+            rids.append(rid)
+        pending, seen = list(rids), []
+        while pending:
+            got = pair.peer.poll_many(pending)
+            seen += got
+            pending = [r for r in pending if r not in got]
+        assert sorted(seen) == sorted(rids)
+        with pytest.raises(kvd.KvdError) as ei:          # retired ids are no longer in flight
+            pair.peer.poll_many(rids[:1])
+        assert ei.value.status == kvd.EINVAL
+        assert pair.peer.poll_many([]) == []
+        exp = pair.dst_host
+        for s, d in tables:
+            exp = pair.expected(s, d, exp)
+        assert_layers_equal(pair.download_dst(), exp)
+    finally:
+        pair.close()
