@@ -127,6 +127,10 @@ _lib.kvd_last_error.argtypes = []
 _lib.kvd_last_error.restype = ctypes.c_char_p
 _lib.kvd_abi_version.argtypes = []
 _lib.kvd_abi_version.restype = ctypes.c_int
+ABI_VERSION = 1     # include/kvd.h KVD_ABI_VERSION this binding was written against
+if _lib.kvd_abi_version() != ABI_VERSION:
+    raise ImportError(f"{LIB_PATH} has ABI {_lib.kvd_abi_version()}, the binding expects "
+                      f"{ABI_VERSION}: rebuild it (__graft_entry__.build())")
 
 
 def _check(status: int, where: str) -> int:
