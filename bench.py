@@ -275,6 +275,25 @@ def run_reference(args, rank, world):
 # the pull arm
 # ---------------------------------------------------------------------------
 
+def nvlink_rx_from_profile(config: str):
+    """NVLink receive counters of the decode GPU from the committed ncu
+    summary (profiles/ncu_pull_<config>_nvlink.json): user data vs total
+    bytes per launch and their rates over the profiled kernel's duration."""
+    p = os.path.join(ROOT, "profiles", f"ncu_pull_{config}_nvlink.json")
+    try:
+        with open(p) as f:
+            m = json.load(f)["metrics"]
+        t = m["gpu__time_duration.sum"]["value"] * 1e-6
+        user = m["nvlrx__bytes_data_user.sum"]["value"]
+        total = m["nvlrx__bytes.sum"]["value"]
+        return {"user_bytes": int(user), "total_bytes": int(total),
+                "user_gbs": round(user / t / 1e9, 1), "total_gbs": round(total / t / 1e9, 1),
+                "protocol_frac": round(1 - user / total, 4),
+                "source": os.path.relpath(p, ROOT) + " (ncu --set full, one launch, cold)"}
+    except Exception:
+        return None
+
+
 def traffic_from_profile(config: str, nvlink: bool):
     """dram bytes per launch of the pull kernel from the committed ncu
     --set full summary (profiles/ncu_pull_<config>[_nvlink].json), else None.
@@ -288,7 +307,30 @@ def traffic_from_profile(config: str, nvlink: bool):
         return None
 
 
-def nccl_baselines(args, g, reqs, src, dst, role, rank, half, dev, gloo, fingerprint):
+def decode_matches(dst, g, s_ids, d_ids, src_seed, dst_seed, dev, scribble_seed=None):
+    """Element-wise parity of a whole decode cache: layer l must equal its
+    seeded pre-state (seed dst_seed*1000+l, or scribble_seed+l after a
+    baseline scribbled it) with blocks d_ids replaced by the prefill's blocks
+    s_ids (seed src_seed*1000+l), for every layer, K/V plane and byte."""
+    import torch
+    span = dst.span_bytes
+    si = torch.from_numpy(np.ascontiguousarray(s_ids)).long().cuda(dev)
+    di = torch.from_numpy(np.ascontiguousarray(d_ids)).long().cuda(dev)
+    ok = True
+    for l in range(g.num_layers):
+        exp = torch.empty_like(dst.layers[l])
+        kvdgen.torch_fill_random_(exp, (scribble_seed + l) if scribble_seed is not None
+                                  else dst_seed * 1000 + l)
+        srcl = torch.empty_like(dst.layers[l])
+        kvdgen.torch_fill_random_(srcl, src_seed * 1000 + l)
+        exp.view(2, g.num_blocks, span)[:, di] = srcl.view(2, g.num_blocks, span)[:, si]
+        ok = ok and bool(torch.equal(dst.layers[l], exp))
+        del exp, srcl
+    torch.cuda.synchronize(dev)
+    return ok
+
+
+def nccl_baselines(args, g, reqs, src, dst, role, rank, half, dev, gloo, src_seed):
     """The measured baseline (north_star: "NCCL send/recv is kept only as the
     measured baseline"), same caches and block tables as the pull.
 
@@ -300,8 +342,17 @@ def nccl_baselines(args, g, reqs, src, dst, role, rank, half, dev, gloo, fingerp
     N2 = grouped per-segment send/recv (ncclGroupStart/End via
     batch_isend_irecv), no staging: one send/recv per contiguous (layer,
     K/V, run) segment straight between the paged caches (C1/C2/C4 only).
+    N3 = N1 with a BOUNDED communication buffer, the way fig:diff(a) drives
+    it: the block list is cut into chunks, two staging buffers
+    alternate, and chunk k+1 is gathered (prefill) / chunk k-1 scattered
+    (decode) while chunk k is on the wire; swept over chunk sizes.
+    N0 = one contiguous ncclSend/ncclRecv of the same byte count: NCCL's
+    own link ceiling, no paged layout at all (context, not a transfer of
+    the cache).
     Each is timed as host wall per step (max over ranks) and parity-checked
-    (the decode cache is scribbled before each baseline)."""
+    element by element (the decode cache is scribbled before each
+    baseline; N0's received buffer is compared with its regenerated
+    contents)."""
     import torch
     import torch.distributed as dist
     from paper_2501_14743_b200 import kvd
@@ -364,8 +415,63 @@ def nccl_baselines(args, g, reqs, src, dst, role, rank, half, dev, gloo, fingerp
 
         plans.append(("n2_grouped_segment_send_recv", n2, max(3, min(args.steps, 10))))
 
+    unit = g.num_layers * 2 * span                 # bytes of one block, all layers and K/V
+
+    def n3(cb):
+        bounds = [(a, min(a + cb, n)) for a in range(0, n, cb)]
+        bufs = [staging[:cb * unit], staging[cb * unit:2 * cb * unit]]
+
+        def fn():
+            works = []
+            if role == "decode":
+                ids_dev.copy_(ids_host, non_blocking=True)
+                dist.send(ids_dev, peer_rank)
+                for k, (a, b) in enumerate(bounds):
+                    # the NCCL stream waits for the current stream here, i.e.
+                    # for the scatter of chunk k-2 that read this buffer
+                    works.append(dist.irecv(bufs[k % 2][:(b - a) * unit], peer_rank))
+                    if k >= 1:
+                        works[k - 1].wait()        # current stream after recv k-1
+                        pa, pb = bounds[k - 1]
+                        kvd.kvd_scatter(dst.handle, d_ids[pa:pb], bufs[(k - 1) % 2].data_ptr(),
+                                        stream.cuda_stream)
+                works[-1].wait()
+                pa, pb = bounds[-1]
+                kvd.kvd_scatter(dst.handle, d_ids[pa:pb], bufs[(len(bounds) - 1) % 2].data_ptr(),
+                                stream.cuda_stream)
+            else:
+                dist.recv(ids_dev, peer_rank)
+                want = ids_dev.cpu().numpy()
+                for k, (a, b) in enumerate(bounds):
+                    if k >= 2:
+                        works[k - 2].wait()        # send k-2 has read this buffer
+                    kvd.kvd_gather(src.handle, want[a:b], bufs[k % 2].data_ptr(),
+                                   stream.cuda_stream)
+                    works.append(dist.isend(bufs[k % 2][:(b - a) * unit], peer_rank))
+                for w in works:
+                    w.wait()
+            torch.cuda.synchronize(dev)
+        return fn
+
+    chunk_sizes = sorted({max(1, (mib << 20) // unit) for mib in (64, 256, 1024)})
+    for cb in chunk_sizes:
+        if 2 * cb <= n:
+            plans.append((f"n3_pipelined_{cb}_blocks", n3(cb), max(3, min(args.steps, 10))))
+
+    def n0():
+        if role == "decode":
+            dist.recv(staging, peer_rank)
+        else:
+            dist.send(staging, peer_rank)
+        torch.cuda.synchronize(dev)
+
+    plans.append(("n0_raw_contiguous", n0, max(3, min(args.steps, 10))))
+
     for name, fn, steps in plans:
         scribble()
+        if name.startswith("n0") and role == "prefill":
+            kvdgen.torch_fill_random_(staging, 4242)
+            torch.cuda.synchronize(dev)
         for _ in range(2):
             fn()
         dist.barrier()
@@ -378,14 +484,18 @@ def nccl_baselines(args, g, reqs, src, dst, role, rank, half, dev, gloo, fingerp
         wall = time.perf_counter() - t0
         dist.barrier()
         ok = True
-        mine = fingerprint(src, s_ids) if role == "prefill" else None
-        fps = [None] * dist.get_world_size()
-        dist.all_gather_object(fps, mine, group=gloo)
         if role == "decode":
-            ok = bool(torch.equal(fingerprint(dst, d_ids), fps[peer_rank]))
+            if name.startswith("n0"):
+                exp = torch.empty_like(staging)
+                kvdgen.torch_fill_random_(exp, 4242)
+                ok = bool(torch.equal(exp, staging))
+                del exp
+            else:
+                ok = decode_matches(dst, g, s_ids, d_ids, src_seed, None, dev, scribble_seed=777)
         out[name] = {"wall_s": wall, "steps": steps, "bytes": per * steps if role == "decode" else 0,
                      "lat": lat, "ok": ok,
-                     "segments": len(seg_views) if name.startswith("n2") else 1}
+                     "segments": (len(seg_views) if name.startswith("n2") else
+                                  -(-n // int(name.split("_")[2])) if name.startswith("n3") else 1)}
     del staging
     return out
 
@@ -507,7 +617,7 @@ def run_kvd(args, rank, world, local_rank):
 
     K = args.steps
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(K)] if peer else []
+          for _ in range(K)] if peer and args.timing == "events" else []
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     lat_ns = []
@@ -526,7 +636,9 @@ def run_kvd(args, rank, world, local_rank):
         if peer:
             t_start.record(stream)
             for k in range(K):
-                issue(ev[k] if not args.streams else None)
+                # timer mode: no events between launches (they would keep
+                # programmatic dependent launch from overlapping consecutive pulls)
+                issue(ev[k] if args.timing == "events" and not args.streams else None)
                 if len(pending) > 768:
                     retire(512)
             if args.streams:
@@ -544,75 +656,90 @@ def run_kvd(args, rank, world, local_rank):
     gt_ms_total, gt_launches = peer.device_time() if peer else (0.0, 0)
     if peer:
         peer.set(kvd.OPT_TIMING, 0)
-    # Per-request transfer latency (R16): issue -> completion observed, one
-    # step at a time on an otherwise idle pair, after the timed region.
-    if peer:
-        for _ in range(max(3, min(K, 50 if n_req == 1 else 5))):
-            step(lat_ns)
-        if args.streams:
-            peer.set(kvd.OPT_STREAMS, 0)   # parity check and calibration in stream order
+    # Per-request transfer latency (R16, SURVEY §8 d), after the timed region:
+    # ISOLATED requests -- issue -> completion observed (kvd_wait_done's
+    # C-side spin on the slot word) -> next, on an otherwise idle pair; all
+    # pairs start each request together (gloo barrier), so for C4 the shards
+    # of one request are pulled concurrently and its latency is the max over
+    # the shard ranks.  C3 also reports the latency of requests queued as in
+    # the timed steps (issue the pair's 16, retire as they land).
+    if args.streams and peer:
+        peer.set(kvd.OPT_STREAMS, 0)   # latency, parity and calibration in stream order
+    reps = max(3, min(K, 50 if n_req == 1 else 3))
+    for _ in range(reps):
+        for s_, d_ in reqs:
+            if multi:
+                dist.barrier(group=gloo)
+            if peer:
+                rid[0] += 1
+                t0 = time.perf_counter_ns()
+                peer.pull(rid[0], s_, d_, stream)
+                peer.wait(rid[0])
+                lat_ns.append(time.perf_counter_ns() - t0)
+    lat_queued = []
+    if peer and n_req > 1:
+        for _ in range(3):
+            step(lat_queued)
 
     info = peer.info() if peer else {}
     dev_s = t_start.elapsed_time(t_end) / 1e3 if peer else 0.0
-    step_ms = ([a.elapsed_time(b) for a, b in ev] if not args.streams
+    step_ms = ([a.elapsed_time(b) for a, b in ev] if args.timing == "events" and not args.streams
                else [dev_s * 1e3 / K] if peer else [])
     span = (src or dst).span_bytes
     bytes_per_step = n_blocks * g.num_layers * 2 * span
 
-    # parity of the timed configuration (checked once, after timing)
+    # parity of the timed configuration (checked once, after timing),
+    # element by element: every layer of the decode cache must equal the
+    # plain definition of the result (SURVEY §8 c) -- its own seeded
+    # pre-state with the requested blocks replaced by the prefill's blocks,
+    # both regenerated here from their torch-generator seeds.
     s_all = np.concatenate([s for s, _ in reqs])
     d_all = np.concatenate([d for _, d in reqs])
-
-    def fp(cache, ids):
-        idx = torch.from_numpy(np.ascontiguousarray(ids)).long().cuda(dev)
-        w = torch.arange(1, cache.span_bytes // 8 + 1, device=f"cuda:{dev}", dtype=torch.int64)
-        return torch.stack([(cache.layers[l].view(2, g.num_blocks, -1)[:, idx]
-                             .view(torch.int64) * w).sum(-1)
-                            for l in range(g.num_layers)]).cpu()
-
+    src_seed = 1 + (me.peer if multi else rank)
     ok = True
-    if role == "both":
-        si = torch.from_numpy(s_all).long().cuda(dev)
-        di = torch.from_numpy(d_all).long().cuda(dev)
-        for l in range(g.num_layers):
-            ok = ok and torch.equal(dst.layers[l].view(2, g.num_blocks, span)[:, di],
-                                    src.layers[l].view(2, g.num_blocks, span)[:, si])
-    if multi:
-        # prefill ranks publish per-(layer, plane, block) fingerprints of the
-        # requests' source blocks; decode ranks compare their destination blocks
-        fps = [None] * world
-        dist.all_gather_object(fps, fp(src, s_all) if role == "prefill" else None, group=gloo)
-        if role == "decode":
-            ok = bool(torch.equal(fp(dst, d_all), fps[me.peer]))
+    if role in ("decode", "both"):
+        ok = decode_matches(dst, g, s_all, d_all, src_seed, 100 + rank, dev)
     oks = [None] * world if multi else [ok]
     if multi:
         dist.all_gather_object(oks, bool(ok), group=gloo)
 
-    # Context (after the parity check, it overwrites destination blocks): the
-    # copy engine over the same mapping (cudaMemcpyAsync per segment,
-    # KVD_VARIANT_CE) on a contiguous request as large as the first request.
-    ce_gbs = None
+    # Link-ceiling calibration (SURVEY §8 d; after the parity check, it
+    # overwrites destination blocks): a CONTIGUOUS request as large as the
+    # first request of a step, (i) read by the TMA bulk-copy ring on every SM
+    # (the SM/TMA contiguous peer-read ceiling) and (ii) copied by the copy
+    # engine over the same mapping (one cudaMemcpyAsync per (layer, K/V)
+    # segment, KVD_VARIANT_CE).  The better of the two is the measured
+    # denominator of the N >= 2 roofline.
+    ce_gbs = tma_gbs = None
     if peer and args.config != "c1":
         n0 = min(len(reqs[0][0]), g.num_blocks)
         cs, cd = kvdgen.contiguous_table(n0, 0, g.num_blocks - n0)
-        peer.set(kvd.OPT_VARIANT, kvd.VARIANT_CE)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        rid[0] += 1
-        peer.pull(rid[0], cs, cd, stream)
-        peer.wait(rid[0])
-        e0.record(stream)
-        for _ in range(3):
+
+        def timed_contiguous(reps=3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             rid[0] += 1
             peer.pull(rid[0], cs, cd, stream)
             peer.wait(rid[0])
-        e1.record(stream)
-        torch.cuda.synchronize()
-        ce_gbs = 3 * n0 * g.num_layers * 2 * span / (e0.elapsed_time(e1) / 1e3) / 1e9
-        peer.set(kvd.OPT_VARIANT, {"lsu": 1, "lsu32": 2, "ce": 3, "tma": 4}.get(args.variant, 0))
+            e0.record(stream)
+            for _ in range(reps):
+                rid[0] += 1
+                peer.pull(rid[0], cs, cd, stream)
+            e1.record(stream)
+            peer.wait(rid[0])
+            torch.cuda.synchronize()
+            return reps * n0 * g.num_layers * 2 * span / (e0.elapsed_time(e1) / 1e3) / 1e9
+
+        peer.set(kvd.OPT_VARIANT, kvd.VARIANT_CE)
+        ce_gbs = timed_contiguous()
+        if multi:
+            peer.set(kvd.OPT_VARIANT, kvd.VARIANT_TMA).set(kvd.OPT_MAX_CTAS, 1 << 16)
+            peer.set(kvd.OPT_THREADS, 32).set(kvd.OPT_STAGES, 6).set(kvd.OPT_TILE_BYTES, 32768)
+            tma_gbs = timed_contiguous()   # (the peer is only closed after this)
 
     base = {}
     if multi and not args.no_nccl:
-        base = nccl_baselines(args, g, reqs, src, dst, role, rank, half, dev, gloo, fp)
+        base = nccl_baselines(args, g, reqs, src, dst, role, rank, half, dev, gloo,
+                              src_seed)
 
     stats = {"dev_s": dev_s, "wall_s": wall if peer else 0.0,
              "bytes": bytes_per_step * K if peer else 0,
@@ -625,6 +752,7 @@ def run_kvd(args, rank, world, local_rank):
              "gt_ms_total": gt_ms_total, "gt_launches": gt_launches,
              "lat": lat_ns, "clock": sampler.summary(), "info": info, "base": base,
              "launches": timed_launches, "runs": info.get("runs"), "ce_gbs": ce_gbs,
+             "tma_gbs": tma_gbs, "lat_queued": lat_queued,
              "bytes_per_step": bytes_per_step if peer else 0}
     all_stats = cluster.gather_stats(stats, gloo) if multi else [stats]
 
@@ -633,6 +761,10 @@ def run_kvd(args, rank, world, local_rank):
         agg = cluster.aggregate(all_stats)          # max time / sum bytes over ranks
         t_dev, t_wall, total = agg["dev_s"], agg["wall_s"], agg["bytes"]
         lat_all = [x for s in dec for x in s["lat"]]
+        # C4: one request = one block table pulled by every TP shard pair at
+        # once; its latency is the slowest shard's (SURVEY §8 d)
+        lat_req = ([max(col) for col in zip(*[s["lat"] for s in dec])]
+                   if args.config == "c4" and len(dec) > 1 else lat_all)
         step_dev = max(s["step_ms"] for s in dec)
         info0 = dec[0]["info"]
         peaks, peak_src = measured_peaks()
@@ -643,15 +775,25 @@ def run_kvd(args, rank, world, local_rank):
         achieved_link = float(np.mean(per_pair))
         bytes_per_step = dec[0]["bytes_per_step"]
         if multi:
+            # denominator: the ceiling measured in this run on contiguous data
+            # (TMA on every SM, or the copy engine, whichever is higher), else
+            # the guide's measured peer copy
+            calib = [max(s["tma_gbs"] or 0.0, s["ce_gbs"] or 0.0) for s in dec]
+            measured = float(np.mean(calib)) if all(calib) else None
+            peak = measured or NVLINK_MEASURED_GBS
             roof = {"bound": "nvlink", "achieved": round(achieved_link, 1),
-                    "peak": NVLINK_MEASURED_GBS, "unit": "GB/s",
-                    "frac": round(achieved_link / NVLINK_MEASURED_GBS, 4),
+                    "peak": round(peak, 1), "unit": "GB/s",
+                    "frac": round(achieved_link / peak, 4),
+                    "peak_source": ("measured in this run: contiguous request of the same size, "
+                                    "best of the TMA ring on every SM and the copy engine "
+                                    "(see calibration)") if measured else
+                                   "B200_PROFILING.md measured peer copy per direction",
+                    "frac_of_guide_770": round(achieved_link / NVLINK_MEASURED_GBS, 4),
                     "frac_of_nominal_900": round(achieved_link / NVLINK_NOMINAL_GBS, 4),
-                    "peak_source": "B200_PROFILING.md measured peer copy per direction "
-                                   "(nominal 900)",
                     "algorithmic_bytes_per_step": bytes_per_step,
                     "per_pair_achieved": [round(x, 1) for x in per_pair],
-                    "traffic": traffic_from_profile(args.config, True)}
+                    "traffic": traffic_from_profile(args.config, True),
+                    "nvlink_rx": nvlink_rx_from_profile(args.config)}
             if all(s["gt_launches"] for s in dec):
                 gt = [s["bytes"] / (s["gt_ms_total"] / 1e3) / 1e9 for s in dec]
                 roof["globaltimer_cross_check"] = {
@@ -707,8 +849,25 @@ def run_kvd(args, rank, world, local_rank):
             # loopback never touches NVLink: no link fraction there
             "frac_of_nvlink_900_per_pair": (round(total / pairs / t_dev / 1e9 /
                                                   NVLINK_NOMINAL_GBS, 4) if multi else None),
-            "p50_latency_ms": round(nearest_rank(lat_all, 50) / 1e6, 4),
-            "p90_latency_ms": round(nearest_rank(lat_all, 90) / 1e6, 4),
+            "p50_latency_ms": round(nearest_rank(lat_req, 50) / 1e6, 4),
+            "p90_latency_ms": round(nearest_rank(lat_req, 90) / 1e6, 4),
+            "latency": {
+                "what": ("isolated requests: host wall from kvd_pull entry to kvd_wait_done "
+                         "observing the completion word, one request at a time on an idle pair, "
+                         "all pairs starting each request together"
+                         + ("; per request the MAX over the TP-shard ranks"
+                            if args.config == "c4" and len(dec) > 1 else "")),
+                "requests_timed": len(lat_req),
+                "per_pair_pooled_p50_ms": round(nearest_rank(lat_all, 50) / 1e6, 4),
+                "queued_p50_ms": (round(nearest_rank([x for s in dec for x in s["lat_queued"]],
+                                                     50) / 1e6, 4)
+                                  if dec[0]["lat_queued"] else None),
+                "queued_p90_ms": (round(nearest_rank([x for s in dec for x in s["lat_queued"]],
+                                                     90) / 1e6, 4)
+                                  if dec[0]["lat_queued"] else None),
+                "queued_what": ("the pair's requests issued together as in a timed step, "
+                                "issue -> completion observed (includes queueing)")
+                               if dec[0]["lat_queued"] else None},
             "step_device_ms": round(step_dev, 4),
             "kernel_ms_per_step": round(kern_dev, 4),
             "roofline": roof,
@@ -720,33 +879,48 @@ def run_kvd(args, rank, world, local_rank):
             "calibration": {
                 "copy_engine_gbs_per_pair": (round(float(np.mean([s["ce_gbs"] for s in dec])), 1)
                                              if all(s["ce_gbs"] for s in dec) else None),
-                "what": "copy engine: cudaMemcpyAsync per (layer, K/V) segment over the same "
-                        "mapping, contiguous request as large as the first request of a step; "
-                        "context for the link ceiling, not the product path (one large peer "
-                        "copy_ tops out at ~779 GB/s on these boxes, tools/ce_probe.py)"},
+                "tma_contiguous_gbs_per_pair": (
+                    round(float(np.mean([s["tma_gbs"] for s in dec])), 1)
+                    if all(s["tma_gbs"] for s in dec) else None),
+                "what": "a contiguous request as large as the first request of a step over the "
+                        "same mapping: (copy engine) one cudaMemcpyAsync per (layer, K/V) "
+                        "segment; (tma) the TMA bulk-copy ring on every SM, 6 x 32 KiB stages "
+                        "per CTA -- the link ceiling the paged pull is measured against"},
             "parity": bool(all(oks)),
             "clocks": clk,
         }
         if multi and not args.no_nccl:
             nb_out = {}
-            for name in ("n1_gather_send_recv_scatter", "n2_grouped_segment_send_recv"):
-                rs = [s["base"][name] for s in all_stats
-                      if s["base"] and name in s["base"] and s["base"][name]["bytes"]]
+            names = sorted({k for s_ in all_stats if s_["base"] for k in s_["base"]})
+            for name in names:
+                rs = [s_["base"][name] for s_ in all_stats
+                      if s_["base"] and name in s_["base"] and s_["base"][name]["bytes"]]
                 if not rs:
                     continue
                 t = max(r["wall_s"] for r in rs)
                 tot = sum(r["bytes"] for r in rs)
                 lat = [x for r in rs for x in r["lat"]]
-                oks_b = [s["base"][name]["ok"] for s in all_stats if s["base"] and name in s["base"]]
+                oks_b = [s_["base"][name]["ok"] for s_ in all_stats
+                         if s_["base"] and name in s_["base"]]
                 nb_out[name] = {"value": round(tot / t / 1e9, 2), "unit": "GB/s",
                                 "gbs_per_pair": round(tot / pairs / t / 1e9, 2),
                                 "p50_step_latency_ms": round(nearest_rank(lat, 50) * 1e3, 4),
-                                "steps": rs[0]["steps"], "segments_per_step": rs[0]["segments"],
+                                "steps": rs[0]["steps"], "messages_per_step": rs[0]["segments"],
                                 "parity": bool(all(oks_b))}
-            nb_out["kvd_pull_e2e_vs_n1"] = round(
-                out["e2e"]["value"] / nb_out["n1_gather_send_recv_scatter"]["value"], 3)
+            transfers = {k: v for k, v in nb_out.items() if not k.startswith("n0")}
+            best = max(transfers, key=lambda k: transfers[k]["value"])
+            nb_out["best_transfer"] = best
+            nb_out["kvd_pull_vs_best_transfer"] = round(out["value"] / nb_out[best]["value"], 3)
+            nb_out["kvd_pull_e2e_vs_best_transfer"] = round(
+                out["e2e"]["value"] / nb_out[best]["value"], 3)
+            if "n0_raw_contiguous" in nb_out:
+                nb_out["kvd_pull_vs_n0_link_ceiling"] = round(
+                    out["value"] / nb_out["n0_raw_contiguous"]["value"], 3)
             nb_out["what"] = ("NCCL 2.28 send/recv via torch.distributed on the same caches and "
-                              "block tables; host wall per step incl. the block-id message")
+                              "block tables; host wall per step incl. the block-id message "
+                              "(N1 whole request staged; N2 one message per segment; N3 "
+                              "double-buffered chunks; N0 one contiguous message of the same "
+                              "bytes, no paged layout = NCCL's link ceiling)")
             out["nccl_baseline"] = nb_out
         if not multi and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_oracle_sample()

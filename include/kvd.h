@@ -26,6 +26,15 @@
  *     CUDA device.
  *   - Entry points marked [host-only] make no CUDA call and work on a
  *     machine without a GPU.
+ *   - Threading (SURVEY §8 b): calls that issue transfers or change a peer
+ *     (kvd_pull, kvd_pull_batch, kvd_push, kvd_peer_set, ...) are serialised
+ *     per peer by an internal mutex; different peers are independent.
+ *     kvd_poll_done, kvd_poll_many and kvd_wait_done take NO lock and make
+ *     no CUDA call: a decode thread polling completions never waits behind
+ *     another thread's validation, planning or kernel launch (P:L380-382:
+ *     completions never block reads).  If several threads poll the same
+ *     request concurrently exactly one of them reports it done.
+ *     kvd_poll_released (exporter side) makes no CUDA call.
  */
 #ifndef KVD_H
 #define KVD_H
@@ -37,7 +46,7 @@
 extern "C" {
 #endif
 
-#define KVD_ABI_VERSION 1
+#define KVD_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define KVD_API __attribute__((visibility("default")))
@@ -145,7 +154,7 @@ typedef enum {
                                (kvd_peer_device_time).  2: the %globaltimer spans only (no events
                                between launches, so back-to-back pulls still overlap launch and
                                tail).  0 (default) off */
-  KVD_OPT_STREAMS = 8       /* 0 or 1 (default): every transfer runs on the caller's stream, in
+  KVD_OPT_STREAMS = 8,      /* 0 or 1 (default): every transfer runs on the caller's stream, in
                                stream order.  k in [2, 8]: a transfer still waits for the work
                                already on the caller's stream, but runs on the next of k library
                                streams, so consecutive transfers overlap (their launch, ramp and
@@ -154,6 +163,15 @@ typedef enum {
                                kvd_wait_done (the paper's decode worker polls) or order a
                                stream after it with kvd_stream_wait.  Changing it synchronises the
                                library streams */
+  KVD_OPT_EARLY_LOADS = 9   /* 1 (default): a pull over NVLink with the TMA mover reads its first
+                               ring of SOURCE blocks before the preceding kernel on the stream
+                               has finished (programmatic dependent launch), so consecutive
+                               pulls overlap ramp and tail; its stores into the decode cache
+                               still wait for that kernel.  The caller guarantees that the
+                               source blocks are not written by work queued earlier on the same
+                               stream (in the paper's flow they are the prefill worker's
+                               finished cache, written by another process).  0: every
+                               access waits (strict stream order) */
 } kvd_option;
 
 typedef struct kvd_cache_s* kvd_cache;
@@ -294,7 +312,9 @@ KVD_API kvd_status kvd_peer_set(kvd_peer peer, int option, int64_t value);
  * dst_ids[i] of the decode cache, bit for bit.  Validates (KVD_ERANGE,
  * KVD_EINVAL) and coalesces on the host, then issues exactly ONE kernel
  * launch on `stream` ("post ... without block") and returns without
- * waiting.  On any error nothing is launched and no byte changes.
+ * waiting.  Stream order: the pull's stores into the decode cache follow
+ * all earlier work on `stream`; over NVLink it may start READING the source
+ * blocks before that work has finished (KVD_OPT_EARLY_LOADS, default on).  On any error nothing is launched and no byte changes.
  * request_id must not be in flight on this peer (KVD_EBUSY).  n = 0 is
  * valid: a flag-only launch; the request completes with no bytes moved. */
 KVD_API kvd_status kvd_pull(kvd_peer peer, uint64_t request_id, const int32_t* src_ids,
@@ -304,8 +324,10 @@ KVD_API kvd_status kvd_pull(kvd_peer peer, uint64_t request_id, const int32_t* s
  * once every byte of the request has landed in decode HBM and is visible
  * to later work on the decode GPU and to the host; the request is then
  * retired (its id may be reused; a later poll of it returns KVD_EINVAL).
- * *done = 0 while in flight.  Makes no CUDA call (reads a pinned flag).
- * Errors: KVD_EINVAL for an unknown request id. */
+ * *done = 0 while in flight.  Lock-free and makes no CUDA call: a lookup in
+ * the peer's request -> slot table, an acquire load of the pinned slot word
+ * and a compare-and-swap to retire.  Errors: KVD_EINVAL for an unknown
+ * request id (or one a concurrent poll just retired). */
 KVD_API kvd_status kvd_poll_done(kvd_peer peer, uint64_t request_id, int* done);
 
 /* Batched drain (§4.2 "Tensor communication",
@@ -341,14 +363,19 @@ KVD_API kvd_status kvd_push(kvd_peer peer, uint64_t request_id, const int32_t* s
  * Complete() message, it notifies the inference engine to release the KV
  * cache block"; P:L375 the request ID is written into the prefill's memory
  * one-sidedly).  Every pull from an exported cache, on completion, posts its
- * request_id into a mailbox in the EXPORTER's device memory (a system-scope
- * atomic claims a slot over NVLink, then a release store publishes it).
- * Called on the exporter's cache, this copies up to `cap` newly completed
- * request ids into `request_ids` (in completion order) and sets *n; the
- * caller may then reuse those source blocks.  Each id is returned once.  The
- * mailbox holds 4096 notifications: poll at least that often, else
- * KVD_EBUSY reports lost notifications.  Synchronous (one small
- * device-to-host copy); returns *n = 0 before the first export. */
+ * request_id into a mailbox in the EXPORTER's host memory: a memfd created
+ * at the first kvd_export_handle, which each importer maps (pidfd_getfd;
+ * same node), registers with CUDA and owns one ring of (64 importers per
+ * exporter at a time).  The completing CTA writes the id at the ring
+ * position its host assigned in issue order -- two plain 64-bit stores over
+ * PCIe, no atomic over NVLink.  Called on the exporter's cache, this copies
+ * up to `cap` newly completed request ids into `request_ids` and sets *n;
+ * the caller may then reuse those source blocks.  Each id is returned once;
+ * per importer in issue order (a request whose pull completes before an
+ * earlier-issued one of the same importer is reported after it).  Each
+ * ring holds 4096 notifications: poll at least that often, else KVD_EBUSY
+ * reports lost notifications.  Plain loads, no CUDA call; *n = 0 before the
+ * first export. */
 KVD_API kvd_status kvd_poll_released(kvd_cache exporter, uint64_t* request_ids, uint32_t cap,
                                      uint32_t* n);
 
@@ -357,8 +384,9 @@ KVD_API kvd_status kvd_wait_done(kvd_peer peer, uint64_t request_id, int64_t tim
 
 /* kvd_poll_done over n in-flight requests in one call (a decode loop admitting
  * many requests): done[i] = 1 and the request retired when it completed, else
- * 0; *ndone = how many completed.  KVD_EINVAL for a request not in flight
- * (entries before it have been processed).  Makes no CUDA call. */
+ * 0; *ndone = how many completed.  All or nothing on bad input: if any id is
+ * not in flight or appears twice, KVD_EINVAL is returned before any request
+ * is retired (*ndone = 0, done[] unspecified).  Lock-free, no CUDA call. */
 KVD_API kvd_status kvd_poll_many(kvd_peer peer, const uint64_t* request_ids, uint32_t n,
                                  uint8_t* done, uint32_t* ndone);
 

@@ -13,6 +13,9 @@
 #include "../../include/kvd.h"
 
 #include <cuda_runtime.h>
+#include <errno.h>
+#include <sys/mman.h>
+#include <sys/syscall.h>
 #include <unistd.h>
 
 #include <algorithm>
@@ -209,7 +212,7 @@ struct Planner {
 // a2: blob codec (little-endian, fixed width)
 // ===========================================================================
 constexpr uint32_t kMagic = 0x4244564bu;  // "KVDB"
-constexpr uint32_t kBlobVersion = 3;
+constexpr uint32_t kBlobVersion = 4;
 
 // One exported allocation: a legacy CUDA IPC handle (cudaMalloc memory) or a
 // VMM shareable handle (kvd_mem_alloc memory: POSIX fd or fabric, §8 f3).
@@ -237,7 +240,8 @@ struct Blob {
   std::vector<BlobAlloc> allocs;
   std::vector<BlobLayer> layers;
   bool has_mbox = false;          // release mailbox (Complete() -> prefill)
-  BlobAlloc mbox{};
+  uint32_t mbox_fd = 0;           // exporter's memfd of the mailbox (host memory)
+  uint64_t mbox_bytes = 0;
 };
 
 struct Writer {
@@ -284,7 +288,11 @@ std::vector<uint8_t> encode_blob(const Blob& B) {
     w.u64(l.offset);
   }
   w.u32(B.has_mbox ? 1u : 0u);
-  if (B.has_mbox) put(B.mbox);
+  if (B.has_mbox) {
+    w.u32(B.mbox_fd);
+    w.u32(0);
+    w.u64(B.mbox_bytes);
+  }
   w.u32(kMagic);  // trailer
   return w.b;
 }
@@ -329,8 +337,11 @@ kvd_status decode_blob(const void* data, size_t len, Blob* B) {
   const uint32_t has_mbox = r.u32();
   if (has_mbox > 1) return fail(KVD_EHANDLE, "blob: bad mailbox flag");
   B->has_mbox = has_mbox == 1;
-  if (B->has_mbox && (!get(B->mbox) || B->mbox.rec.kind != kvd::vmm::kLegacyIpc))
-    return fail(KVD_EHANDLE, "blob: bad mailbox handle kind");
+  if (B->has_mbox) {
+    B->mbox_fd = r.u32();
+    r.u32();
+    B->mbox_bytes = r.u64();
+  }
   if (r.u32() != kMagic || !r.ok) return fail(KVD_EHANDLE, "blob: bad trailer");
   if (r.i != len) return fail(KVD_EHANDLE, "blob: %zu trailing bytes", len - r.i);
   return KVD_OK;
@@ -432,6 +443,100 @@ bool alloc_range(uint64_t addr, uint64_t* base, uint64_t* size) {
   return true;
 }
 
+// ===========================================================================
+// a6, prefill side: the release mailbox.  Host memory (a
+// memfd) owned by the exporter; every importer maps it, registers it with
+// CUDA and claims one single-producer ring (layout: kvd_internal.h).  The
+// exporter's host reads it with plain loads.
+// ===========================================================================
+#ifndef SYS_pidfd_open
+#define SYS_pidfd_open 434
+#endif
+#ifndef SYS_pidfd_getfd
+#define SYS_pidfd_getfd 438
+#endif
+constexpr size_t kMailboxBytes = (kvd::kMailboxWords * sizeof(uint64_t) + 4095) / 4096 * 4096;
+
+uint64_t* mbox_owner(uint64_t* m, uint32_t r) { return m + 8 + 2 * (size_t)r; }
+uint64_t* mbox_next(uint64_t* m, uint32_t r) { return m + 8 + 2 * (size_t)r + 1; }
+uint64_t* mbox_ring(uint64_t* m, uint32_t r) {
+  return m + kvd::kMailboxHeaderWords + 2ull * kvd::kReleaseRing * r;
+}
+
+kvd_status mbox_create(int* fd_out, uint64_t** map_out) {
+  const int fd = memfd_create("kvd-release-mailbox", MFD_CLOEXEC);
+  if (fd < 0) return fail(KVD_ENOMEM, "memfd_create(mailbox): %s", strerror(errno));
+  if (ftruncate(fd, (off_t)kMailboxBytes) != 0) {
+    const int e = errno;
+    close(fd);
+    return fail(KVD_ENOMEM, "ftruncate(mailbox): %s", strerror(e));
+  }
+  void* m = mmap(nullptr, kMailboxBytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+  if (m == MAP_FAILED) {
+    const int e = errno;
+    close(fd);
+    return fail(KVD_ENOMEM, "mmap(mailbox): %s", strerror(e));
+  }
+  uint64_t* w = (uint64_t*)m;                 // zero-filled by ftruncate
+  w[1] = kvd::kMailboxRings;
+  w[2] = kvd::kReleaseRing;
+  __atomic_store_n(&w[0], kvd::kMailboxMagic, __ATOMIC_RELEASE);
+  *fd_out = fd;
+  *map_out = w;
+  return KVD_OK;
+}
+
+// Map the exporter's mailbox into this process (its own fd when the
+// exporter is this process, else fetched with pidfd_getfd).
+kvd_status mbox_map(int64_t pid, uint32_t fd_num, bool same_process, uint64_t bytes,
+                    uint64_t** out) {
+  if (bytes != kMailboxBytes)
+    return fail(KVD_EHANDLE, "blob: mailbox of %llu bytes, expected %zu",
+                (unsigned long long)bytes, kMailboxBytes);
+  int fd = -1;
+  if (same_process) {
+    fd = dup((int)fd_num);
+  } else {
+    const long pidfd = syscall(SYS_pidfd_open, (pid_t)pid, 0);
+    if (pidfd < 0)
+      return fail(KVD_EHANDLE, "pidfd_open(exporter %lld) for the mailbox: %s", (long long)pid,
+                  strerror(errno));
+    fd = (int)syscall(SYS_pidfd_getfd, (int)pidfd, (int)fd_num, 0);
+    const int e = errno;
+    close((int)pidfd);
+    if (fd < 0) return fail(KVD_EHANDLE, "pidfd_getfd(mailbox): %s", strerror(e));
+  }
+  if (fd < 0) return fail(KVD_EHANDLE, "dup(mailbox fd): %s", strerror(errno));
+  void* m = mmap(nullptr, kMailboxBytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+  const int e = errno;
+  close(fd);
+  if (m == MAP_FAILED) return fail(KVD_EHANDLE, "mmap(mailbox): %s", strerror(e));
+  uint64_t* w = (uint64_t*)m;
+  if (__atomic_load_n(&w[0], __ATOMIC_ACQUIRE) != kvd::kMailboxMagic ||
+      w[1] != kvd::kMailboxRings || w[2] != kvd::kReleaseRing) {
+    munmap(m, kMailboxBytes);
+    return fail(KVD_EHANDLE, "mailbox: bad header");
+  }
+  *out = w;
+  return KVD_OK;
+}
+
+// Request -> completion slot table, readable without the peer mutex
+// (kvd_poll_done is lock-free, SURVEY §8 b).  Slots double as an
+// open-addressed hash table keyed by request id: a request lives at the first
+// free slot probing linearly from hash(id); max_probe bounds every lookup.
+// state: 0 free; kReserved while the issuing thread fills the slot; the
+// request's token (unique, >= 1) while in flight; kRetiring while the poller
+// that retired it finishes.  Only the issuing thread (holding the peer
+// mutex) moves a slot out of 0; only a poller's compare-and-swap moves it
+// out of a token.
+constexpr uint64_t kReserved = ~0ull;
+constexpr uint64_t kRetiring = ~0ull - 1;
+
+uint32_t slot_hash(uint64_t rid, uint32_t nslots) {
+  return (uint32_t)((rid * 0x9E3779B97F4A7C15ull) >> 40) & (nslots - 1);
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -448,12 +553,10 @@ struct kvd_cache_s {
   std::vector<int4> runs4;
   std::vector<int32_t> iota;
   // release mailbox (exporter side): importers post completed request ids
-  unsigned long long* mbox_dev = nullptr;
-  uint64_t mbox_head = 0;                 // next sequence to consume
-  // the mailbox is read on a private non-blocking stream into pinned memory,
-  // so polling never waits behind the exporter's own (prefill) work
-  cudaStream_t mbox_stream = nullptr;
-  unsigned long long* mbox_pinned = nullptr;
+  // into host memory this process shares with them; polling is plain loads
+  int mbox_fd = -1;
+  uint64_t* mbox = nullptr;
+  uint64_t mbox_head[kvd::kMailboxRings] = {};   // next position to consume, per ring
 };
 
 namespace {
@@ -466,30 +569,39 @@ struct kvd_peer_s {
   int remote_device = -1;
   bool same_process = false;
   std::vector<std::string> opened;         // mapping keys we opened (to close)
-  unsigned long long* mbox = nullptr;       // the exporter's release mailbox, mapped here
+  // the exporter's release mailbox (host memory), mapped and registered here
+  uint64_t* mbox_map = nullptr;
+  uint32_t mbox_ring = 0;                   // the ring this importer claimed
+  uint64_t mbox_owner = 0;                  // its owner word while claimed
+  unsigned long long* mbox = nullptr;       // device pointer to that ring
+  uint64_t mbox_next = 0;                   // ring position of the next request (issue order)
   unsigned long long* d_src_bases = nullptr;
   std::vector<uint64_t> src_bases;         // host copy of the mapped remote layer bases
 
-  // completion slots (a6)
+  // completion slots (a6); request -> slot table (lock-free for pollers)
   unsigned long long* flags = nullptr;      // pinned, host-mapped
   unsigned long long* flags_dev = nullptr;
   unsigned int* counters = nullptr;         // device
-  std::vector<uint64_t> slot_seq;           // 0 = free, else the token in flight
-  uint32_t cursor = 0;
-  uint64_t seq = 0;
-  struct InFlight {
-    uint32_t slot;
-    uint64_t token;
-    int32_t batch;                          // batch descriptor buffer, -1 for single pulls
+  struct Slot {
+    std::atomic<uint64_t> state{0};         // 0 | kReserved | token | kRetiring
+    std::atomic<uint64_t> rid{0};
     bool timed = false;                     // the kernel writes its %globaltimer duration
   };
-  std::unordered_map<uint64_t, InFlight> inflight;
+  std::unique_ptr<Slot[]> slots;
+  std::atomic<uint32_t> max_probe{0};
+  uint64_t seq = 0;
   unsigned long long* bytectr = nullptr;    // device per-slot byte counters (batched drain)
+  // Batched launches: a descriptor buffer is reusable once its kernel has
+  // ENDED (its last CTA released done_seq into *done), not merely once its
+  // requests completed -- the launch's own counters live in the buffer.
+  static constexpr size_t kBatchCtrBytes = 256;   // dev: {arrive, tile} counters, then descriptors
   struct BatchBuf {
-    char* dev = nullptr;                    // runs | reqs | tokens | run_pos
-    char* host = nullptr;                   // pinned staging
-    size_t cap = 0;
-    uint32_t refs = 0;                      // requests of the batch not yet retired
+    char* dev = nullptr;                    // counters | runs | reqs | tokens | ids | run_pos
+    char* host = nullptr;                   // pinned staging of the descriptors
+    size_t cap = 0;                         // descriptor bytes
+    unsigned long long* done = nullptr;     // pinned, host-mapped
+    unsigned long long* done_dev = nullptr;
+    uint64_t seq = 0;                       // value the last launch releases
   };
   std::vector<BatchBuf> batch_bufs;
   std::vector<int4*> slot_runs_dev;         // big run tables (per slot)
@@ -505,6 +617,7 @@ struct kvd_peer_s {
   uint32_t stages = 4;                      // TMA ring depth (auto TMA: 6)
   bool stages_set = false;
   int coalesce = 1;
+  bool early_loads = true;                  // KVD_OPT_EARLY_LOADS
   int variant = KVD_VARIANT_AUTO;
   int sm_count = 148;
 
@@ -521,8 +634,8 @@ struct kvd_peer_s {
   unsigned long long* gt_start = nullptr;   // per-slot earliest CTA start (device, ~0 idle)
   unsigned long long* gt_host = nullptr;    // per-slot duration ns (pinned, host-mapped)
   unsigned long long* gt_dev = nullptr;
-  double gt_total_ms = 0;                   // durations of retired timed requests
-  uint64_t gt_count = 0;
+  std::atomic<uint64_t> gt_ns{0};           // summed durations of retired timed requests
+  std::atomic<uint64_t> gt_count{0};
   // KVD_OPT_STREAMS >= 2: transfers fork off the caller's stream onto these
   uint32_t nstreams = 0;
   std::vector<cudaStream_t> streams;
@@ -685,10 +798,10 @@ static void cache_release(kvd_cache c) {
   if (c->device >= 0) {
     DeviceGuard dg(c->device);
     if (c->d_bases) cudaFree(c->d_bases);
-    if (c->mbox_dev) cudaFree(c->mbox_dev);
-    if (c->mbox_stream) cudaStreamDestroy(c->mbox_stream);
-    if (c->mbox_pinned) cudaFreeHost(c->mbox_pinned);
   }
+  // importers keep their own mappings of the mailbox pages
+  if (c->mbox) munmap(c->mbox, kMailboxBytes);
+  if (c->mbox_fd >= 0) close(c->mbox_fd);
   delete c;
 }
 
@@ -821,27 +934,13 @@ kvd_status kvd_export_handle(kvd_cache c, void* blob, size_t* blob_len) {
   {
     // the release mailbox importers post completed request ids into
     std::lock_guard<std::mutex> lk(c->mu);
-    if (!c->mbox_dev) {
-      KVD_CUDA(cudaMalloc(&c->mbox_dev, kvd::kMailboxWords * sizeof(unsigned long long)));
-      KVD_CUDA(cudaMemset(c->mbox_dev, 0, kvd::kMailboxWords * sizeof(unsigned long long)));
-      KVD_CUDA(cudaDeviceSynchronize());
-      c->mbox_head = 0;
+    if (!c->mbox) {
+      kvd_status ms = mbox_create(&c->mbox_fd, &c->mbox);
+      if (ms != KVD_OK) return ms;
     }
-    if (!c->mbox_stream)
-      KVD_CUDA(cudaStreamCreateWithFlags(&c->mbox_stream, cudaStreamNonBlocking));
-    if (!c->mbox_pinned)
-      KVD_CUDA(cudaMallocHost(&c->mbox_pinned, kvd::kMailboxWords * sizeof(unsigned long long)));
-    cudaIpcMemHandle_t h;
-    cudaError_t e = cudaIpcGetMemHandle(&h, c->mbox_dev);
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      return fail(KVD_EHANDLE, "cudaIpcGetMemHandle(mailbox): %s", cudaGetErrorString(e));
-    }
-    B.mbox.rec.kind = kvd::vmm::kLegacyIpc;
-    memcpy(B.mbox.rec.payload, &h, sizeof(h));
     B.has_mbox = true;
-    B.mbox.base = (uint64_t)(uintptr_t)c->mbox_dev;
-    B.mbox.size = kvd::kMailboxWords * sizeof(unsigned long long);
+    B.mbox_fd = (uint32_t)c->mbox_fd;
+    B.mbox_bytes = kMailboxBytes;
   }
   std::vector<uint8_t> bytes = encode_blob(B);
   const size_t cap = *blob_len;
@@ -859,6 +958,12 @@ static void peer_release(kvd_peer p) {
   // them finish before anything is unmapped or freed (close is not hot)
   if (p->local) cudaDeviceSynchronize();
   for (auto& k : p->opened) map_close(k, p->local->device);
+  if (p->mbox_map) {
+    if (p->mbox_owner)   // hand the ring back (its next position stays in the header)
+      __atomic_store_n(mbox_owner(p->mbox_map, p->mbox_ring), 0ull, __ATOMIC_RELEASE);
+    cudaHostUnregister(p->mbox_map);
+    munmap(p->mbox_map, kMailboxBytes);
+  }
   if (p->d_src_bases) cudaFree(p->d_src_bases);
   if (p->flags) cudaFreeHost(p->flags);
   if (p->counters) cudaFree(p->counters);
@@ -878,6 +983,7 @@ static void peer_release(kvd_peer p) {
   for (auto& b : p->batch_bufs) {
     if (b.dev) cudaFree(b.dev);
     if (b.host) cudaFreeHost(b.host);
+    if (b.done) cudaFreeHost(b.done);
   }
   for (auto q : p->slot_runs_dev) if (q) cudaFree(q);
   for (auto q : p->slot_runs_host) if (q) cudaFreeHost(q);
@@ -971,18 +1077,33 @@ static kvd_status open_impl(kvd_cache local, const void* blob, size_t blob_len,
     }
   }
   if (B.has_mbox) {
-    if (B.mbox.size < kvd::kMailboxWords * sizeof(unsigned long long))
-      return fail(KVD_EHANDLE, "blob: mailbox too small");
-    if (p->same_process) {
-      p->mbox = (unsigned long long*)(uintptr_t)B.mbox.base;
-    } else {
-      void* ptr = nullptr;
-      std::string key;
-      s = map_open(B.mbox, B.pid, B.nonce, local->device, &ptr, &key);
-      if (s != KVD_OK) return s;
-      p->opened.push_back(key);
-      p->mbox = (unsigned long long*)ptr;
+    s = mbox_map(B.pid, B.mbox_fd, p->same_process, B.mbox_bytes, &p->mbox_map);
+    if (s != KVD_OK) return s;
+    cudaError_t e = cudaHostRegister(p->mbox_map, kMailboxBytes,
+                                     cudaHostRegisterMapped | cudaHostRegisterPortable);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      munmap(p->mbox_map, kMailboxBytes);
+      p->mbox_map = nullptr;
+      return fail(KVD_EHANDLE, "cudaHostRegister(mailbox): %s", cudaGetErrorString(e));
     }
+    const uint64_t owner = (process_nonce() ^ (uint64_t)(uintptr_t)p.get()) | 1ull;
+    for (uint32_t r = 0; r < kvd::kMailboxRings && !p->mbox_owner; ++r) {
+      uint64_t expect = 0;
+      if (__atomic_compare_exchange_n(mbox_owner(p->mbox_map, r), &expect, owner, false,
+                                      __ATOMIC_ACQ_REL, __ATOMIC_ACQUIRE)) {
+        p->mbox_ring = r;
+        p->mbox_owner = owner;
+      }
+    }
+    if (!p->mbox_owner)
+      return fail(KVD_EBUSY, "the exporter's release mailbox has no free ring (%u importers open)",
+                  kvd::kMailboxRings);
+    p->mbox_next = __atomic_load_n(mbox_next(p->mbox_map, p->mbox_ring), __ATOMIC_ACQUIRE);
+    void* dev = nullptr;
+    KVD_CUDA(cudaHostGetDevicePointer(&dev, p->mbox_map, 0));
+    p->mbox = (unsigned long long*)((char*)dev + ((char*)mbox_ring(p->mbox_map, p->mbox_ring) -
+                                                  (char*)p->mbox_map));
   }
   std::vector<uint64_t> src(B.layers.size());
   for (size_t l = 0; l < B.layers.size(); ++l) {
@@ -1013,7 +1134,7 @@ static kvd_status open_impl(kvd_cache local, const void* blob, size_t blob_len,
   memset(p->gt_host, 0, kSlots * sizeof(unsigned long long));
   KVD_CUDA(cudaHostGetDevicePointer((void**)&p->gt_dev, p->gt_host, 0));
   KVD_CUDA(cudaDeviceSynchronize());
-  p->slot_seq.assign(kSlots, 0);
+  p->slots.reset(new kvd_peer_s::Slot[kSlots]);
   p->slot_runs_dev.assign(kSlots, nullptr);
   p->slot_runs_host.assign(kSlots, nullptr);
   p->slot_runs_cap.assign(kSlots, 0);
@@ -1057,6 +1178,9 @@ kvd_status kvd_peer_set(kvd_peer p, int option, int64_t value) {
       return KVD_OK;
     case KVD_OPT_COALESCE:
       p->coalesce = value ? 1 : 0;
+      return KVD_OK;
+    case KVD_OPT_EARLY_LOADS:
+      p->early_loads = value != 0;
       return KVD_OK;
     case KVD_OPT_VARIANT:
       if (value < KVD_VARIANT_AUTO || value > KVD_VARIANT_TMA)
@@ -1318,6 +1442,77 @@ static void timing_end(kvd_peer_s* p, cudaStream_t s) {
   if (p->timing_events && !p->timed.empty()) cudaEventRecord(p->timed.back().second, s);
 }
 
+// ---------------------------------------------------------------------------
+// the request -> slot table (see slot_hash); lookups take no lock
+// ---------------------------------------------------------------------------
+static bool slot_find(const kvd_peer_s* p, uint64_t rid, uint32_t* slot, uint64_t* token) {
+  const uint32_t h = slot_hash(rid, kSlots);
+  const uint32_t maxp = p->max_probe.load(std::memory_order_acquire);
+  for (uint32_t d = 0; d <= maxp && d < kSlots; ++d) {
+    const uint32_t i = (h + d) & (kSlots - 1);
+    const kvd_peer_s::Slot& S = p->slots[i];
+    const uint64_t st = S.state.load(std::memory_order_acquire);
+    if (st == 0 || st == kReserved || st == kRetiring) continue;
+    const uint64_t r = S.rid.load(std::memory_order_relaxed);
+    std::atomic_thread_fence(std::memory_order_acquire);
+    if (r != rid || S.state.load(std::memory_order_relaxed) != st) continue;
+    *slot = i;
+    *token = st;
+    return true;
+  }
+  return false;
+}
+
+// Issuing thread only (peer mutex held): take the first free slot on
+// rid's probe sequence and mark it reserved; kSlots if none is free.
+static uint32_t slot_reserve(kvd_peer_s* p, uint64_t rid) {
+  const uint32_t h = slot_hash(rid, kSlots);
+  for (uint32_t d = 0; d < kSlots; ++d) {
+    const uint32_t i = (h + d) & (kSlots - 1);
+    kvd_peer_s::Slot& S = p->slots[i];
+    if (S.state.load(std::memory_order_acquire) != 0) continue;
+    S.state.store(kReserved, std::memory_order_relaxed);
+    S.rid.store(rid, std::memory_order_relaxed);
+    if (d > p->max_probe.load(std::memory_order_relaxed))
+      p->max_probe.store(d, std::memory_order_release);
+    return i;
+  }
+  return kSlots;
+}
+
+// Make a reserved slot visible to pollers (after its kernel was launched).
+static void slot_publish(kvd_peer_s* p, uint32_t i, uint64_t token, bool timed) {
+  p->slots[i].timed = timed;
+  p->slots[i].state.store(token, std::memory_order_release);
+}
+
+static void slot_cancel(kvd_peer_s* p, uint32_t i) {
+  p->slots[i].state.store(0, std::memory_order_release);
+}
+
+// Retire a request whose completion word holds its token; exactly one of
+// several concurrent pollers wins.
+static bool slot_retire(kvd_peer_s* p, uint32_t i, uint64_t token) {
+  kvd_peer_s::Slot& S = p->slots[i];
+  uint64_t expect = token;
+  if (!S.state.compare_exchange_strong(expect, kRetiring, std::memory_order_acq_rel,
+                                       std::memory_order_acquire))
+    return false;
+  if (S.timed) {   // written by the kernel before the slot word's release
+    p->gt_ns.fetch_add(__atomic_load_n(&p->gt_host[i], __ATOMIC_RELAXED), std::memory_order_relaxed);
+    p->gt_count.fetch_add(1, std::memory_order_relaxed);
+  }
+  S.state.store(0, std::memory_order_release);
+  return true;
+}
+
+// Ring position of the next request's release post (issue order).
+static void mbox_commit(kvd_peer_s* p, uint64_t next) {
+  p->mbox_next = next;
+  if (p->mbox_map)
+    __atomic_store_n(mbox_next(p->mbox_map, p->mbox_ring), next, __ATOMIC_RELEASE);
+}
+
 // Pull (push = false): remote (imported) cache -> local cache, kernel on the
 // local GPU reading over NVLink.  Push (push = true, §8 f2): local cache ->
 // remote cache, kernel on the local GPU storing over NVLink.
@@ -1326,8 +1521,12 @@ static kvd_status transfer(kvd_peer p, uint64_t request_id, const int32_t* src_i
   if (!p) return fail(KVD_EINVAL, "null peer");
   std::lock_guard<std::mutex> lk(p->mu);
   if (p->closed) return fail(KVD_ESTATE, "peer closed");
-  if (p->inflight.count(request_id))
-    return fail(KVD_EBUSY, "request %llu already in flight", (unsigned long long)request_id);
+  {
+    uint32_t i;
+    uint64_t t;
+    if (slot_find(p, request_id, &i, &t))
+      return fail(KVD_EBUSY, "request %llu already in flight", (unsigned long long)request_id);
+  }
   const Geom& SG = push ? p->local->geom : p->remote;
   const Geom& DG = push ? p->remote : p->local->geom;
   const kvd_geometry& sg = SG.g;
@@ -1357,13 +1556,15 @@ static kvd_status transfer(kvd_peer p, uint64_t request_id, const int32_t* src_i
     s = tile_runs(p->runs, pp, NL, pol.tile, p->runs4, a);
     if (s != KVD_OK) return s;
   }
-  // a6: completion slot
-  uint32_t slot = kSlots;
-  for (uint32_t k = 0; k < kSlots; ++k) {
-    const uint32_t c = (p->cursor + k) % kSlots;
-    if (p->slot_seq[c] == 0) { slot = c; break; }
-  }
+  // a6: completion slot (reserved now, published after the launch)
+  const uint32_t slot = slot_reserve(p, request_id);
   if (slot == kSlots) return fail(KVD_EBUSY, "all %u completion slots in flight (poll them)", kSlots);
+  struct Cancel {   // every error return below hands the slot back
+    kvd_peer_s* p;
+    uint32_t slot;
+    bool armed = true;
+    ~Cancel() { if (armed) slot_cancel(p, slot); }
+  } cancel{p, slot};
   const uint64_t token = ++p->seq;
   a.counter = p->counters + slot;
   a.flag = p->flags_dev + slot;
@@ -1371,6 +1572,7 @@ static kvd_status transfer(kvd_peer p, uint64_t request_id, const int32_t* src_i
   a.remote_stores = push ? 1u : 0u;
   a.request_id = request_id;
   a.mbox = push ? nullptr : p->mbox;   // Complete() -> the prefill exporter (pull only)
+  a.mbox_pos = p->mbox_next;
   a.audit = p->audit_ctr;
   a.src_layer_bytes = sg.layer_bytes;
   a.dst_layer_bytes = dg_.layer_bytes;
@@ -1391,7 +1593,7 @@ static kvd_status transfer(kvd_peer p, uint64_t request_id, const int32_t* src_i
   info.bytes = (uint64_t)n * NL * 2 * sg.span_bytes;
   cudaError_t e = cudaSuccess;
   if (n == 0) {
-    e = kvd::launch_flag_only(a.flag, token, a.mbox, request_id, stream);
+    e = kvd::launch_flag_only(a.flag, token, a.mbox, a.mbox_pos, request_id, stream);
     info.launches = 1;
     info.ctas = 1;
   } else if (variant == KVD_VARIANT_CE) {
@@ -1410,7 +1612,8 @@ static kvd_status transfer(kvd_peer p, uint64_t request_id, const int32_t* src_i
             ++launches;
           }
         }
-    if (e == cudaSuccess) e = kvd::launch_flag_only(a.flag, token, a.mbox, request_id, stream);
+    if (e == cudaSuccess)
+      e = kvd::launch_flag_only(a.flag, token, a.mbox, a.mbox_pos, request_id, stream);
     info.launches = launches + 1;
     info.segments = launches;
   } else {
@@ -1438,9 +1641,11 @@ static kvd_status transfer(kvd_peer p, uint64_t request_id, const int32_t* src_i
     uint32_t threads = 0, ctas = 0;
     s = launch_shape(p, pol, a, info.bytes, &threads, &ctas);
     if (s != KVD_OK) return s;
-#ifndef KVD_EXPERIMENT_STATIC_TILES
-    if (variant == KVD_VARIANT_TMA && !p->row_bytes) a.tile_ctr = p->tile_ctrs + slot;
-#endif
+    if (variant == KVD_VARIANT_TMA && !p->row_bytes) {
+      a.tile_ctr = p->tile_ctrs + slot;
+      // the next pull's source reads overlap this one's tail
+      a.early_loads = (p->early_loads && !push && p->remote_device != p->local->device) ? 1u : 0u;
+    }
     timing_begin(p, stream);
     e = kvd::launch_pull(a, p->runs4.data(), variant, ctas, threads, pol.stages, stream);
     timing_end(p, stream);
@@ -1452,9 +1657,9 @@ static kvd_status transfer(kvd_peer p, uint64_t request_id, const int32_t* src_i
   }
   if (e != cudaSuccess) return cuda_fail(e, "pull launch");
   info.variant = (uint32_t)variant;
-  p->slot_seq[slot] = token;
-  p->cursor = (slot + 1) % kSlots;
-  p->inflight[request_id] = kvd_peer_s::InFlight{slot, token, -1, timed};
+  if (a.mbox) mbox_commit(p, a.mbox_pos + 1);
+  cancel.armed = false;
+  slot_publish(p, slot, token, timed);
   p->last = info;
   return KVD_OK;
 }
@@ -1485,7 +1690,9 @@ kvd_status kvd_pull_batch(kvd_peer p, uint32_t num_requests, const uint64_t* req
   {
     std::unordered_map<uint64_t, uint32_t> seen;
     for (uint32_t q = 0; q < num_requests; ++q) {
-      if (p->inflight.count(request_ids[q]))
+      uint32_t i;
+      uint64_t t;
+      if (slot_find(p, request_ids[q], &i, &t))
         return fail(KVD_EBUSY, "request %llu already in flight", (unsigned long long)request_ids[q]);
       if (!seen.emplace(request_ids[q], q).second)
         return fail(KVD_EINVAL, "request %llu twice in one batch", (unsigned long long)request_ids[q]);
@@ -1533,32 +1740,65 @@ kvd_status kvd_pull_batch(kvd_peer p, uint32_t num_requests, const uint64_t* req
   if (pol.variant == KVD_VARIANT_LSU32 && !aligned32(a, p->src_bases, p->local->bases))
     pol.variant = KVD_VARIANT_LSU;
 
-  // completion slots, one per request
+  // completion slots, one per request (reserved now, published after the launch)
   std::vector<uint32_t> slots;
-  for (uint32_t k = 0; k < kSlots && slots.size() < num_requests; ++k) {
-    const uint32_t c = (p->cursor + k) % kSlots;
-    if (p->slot_seq[c] == 0) slots.push_back(c);
+  slots.reserve(num_requests);
+  struct Cancel {
+    kvd_peer_s* p;
+    std::vector<uint32_t>* slots;
+    bool armed = true;
+    ~Cancel() {
+      if (armed)
+        for (uint32_t i : *slots) slot_cancel(p, i);
+    }
+  } cancel{p, &slots};
+  for (uint32_t q = 0; q < num_requests; ++q) {
+    const uint32_t i = slot_reserve(p, request_ids[q]);
+    if (i == kSlots)
+      return fail(KVD_EBUSY, "need %u free completion slots (poll finished requests)", num_requests);
+    slots.push_back(i);
   }
-  if (slots.size() < num_requests)
-    return fail(KVD_EBUSY, "need %u free completion slots (poll finished requests)", num_requests);
 
-  // device descriptor block: runs | reqs | tokens | run_pos
+  // device descriptor block: counters | runs | reqs | tokens | ids | run_pos
   const size_t m = p->runs4.size();
   const size_t off_reqs = m * sizeof(int4);
   const size_t off_tok = off_reqs + num_requests * sizeof(uint4);
   const size_t off_ids = off_tok + num_requests * sizeof(unsigned long long);
   const size_t off_pos = off_ids + num_requests * sizeof(unsigned long long);
   const size_t bytes_needed = off_pos + std::max<size_t>(m, 1) * sizeof(uint32_t);
+  constexpr size_t C = kvd_peer_s::kBatchCtrBytes;
   int32_t bi = -1;
-  for (size_t b = 0; b < p->batch_bufs.size(); ++b)
-    if (p->batch_bufs[b].refs == 0 && p->batch_bufs[b].cap >= bytes_needed) { bi = (int32_t)b; break; }
+  for (size_t b = 0; b < p->batch_bufs.size(); ++b) {
+    const kvd_peer_s::BatchBuf& X = p->batch_bufs[b];
+    // idle = the previous launch over this buffer has ended (its last CTA
+    // reset the counters and released seq)
+    if (X.cap >= bytes_needed && __atomic_load_n(X.done, __ATOMIC_ACQUIRE) == X.seq) {
+      bi = (int32_t)b;
+      break;
+    }
+  }
   DeviceGuard dgd(p->local->device);
   if (!dgd.ok) return fail(KVD_ECUDA, "cannot select device %d", p->local->device);
   if (bi < 0) {
     kvd_peer_s::BatchBuf nb;
     nb.cap = std::max<size_t>(bytes_needed, 64 << 10);
-    KVD_CUDA(cudaMalloc(&nb.dev, nb.cap));
-    KVD_CUDA(cudaMallocHost(&nb.host, nb.cap));
+    cudaError_t e = cudaMalloc(&nb.dev, C + nb.cap);
+    if (e == cudaSuccess) e = cudaMemset(nb.dev, 0, C);
+    if (e == cudaSuccess) e = cudaMallocHost(&nb.host, nb.cap);
+    if (e == cudaSuccess)
+      e = cudaHostAlloc((void**)&nb.done, sizeof(unsigned long long),
+                        cudaHostAllocMapped | cudaHostAllocPortable);
+    if (e == cudaSuccess) {
+      *nb.done = 0;
+      e = cudaHostGetDevicePointer((void**)&nb.done_dev, nb.done, 0);
+    }
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();   // counters zeroed before first use
+    if (e != cudaSuccess) {
+      if (nb.dev) cudaFree(nb.dev);
+      if (nb.host) cudaFreeHost(nb.host);
+      if (nb.done) cudaFreeHost(nb.done);
+      return cuda_fail(e, "batch descriptor buffer");
+    }
     p->batch_bufs.push_back(nb);
     bi = (int32_t)p->batch_bufs.size() - 1;
   }
@@ -1582,17 +1822,23 @@ kvd_status kvd_pull_batch(kvd_peer p, uint32_t num_requests, const uint64_t* req
   }
   cudaStream_t stream = nullptr;
   KVD_CUDA(route_stream(p, (cudaStream_t)stream_, &stream));
-  KVD_CUDA(cudaMemcpyAsync(B.dev, B.host, bytes_needed, cudaMemcpyHostToDevice, stream));
-  a.runs_dev = reinterpret_cast<const int4*>(B.dev);
+  char* D = B.dev + C;
+  KVD_CUDA(cudaMemcpyAsync(D, B.host, bytes_needed, cudaMemcpyHostToDevice, stream));
+  a.runs_dev = reinterpret_cast<const int4*>(D);
   a.nreqs = num_requests;
-  a.reqs = reinterpret_cast<const uint4*>(B.dev + off_reqs);
-  a.tokens = reinterpret_cast<const unsigned long long*>(B.dev + off_tok);
-  a.run_pos = reinterpret_cast<const unsigned int*>(B.dev + off_pos);
-  a.req_ids = reinterpret_cast<const unsigned long long*>(B.dev + off_ids);
+  a.reqs = reinterpret_cast<const uint4*>(D + off_reqs);
+  a.tokens = reinterpret_cast<const unsigned long long*>(D + off_tok);
+  a.run_pos = reinterpret_cast<const unsigned int*>(D + off_pos);
+  a.req_ids = reinterpret_cast<const unsigned long long*>(D + off_ids);
   a.mbox = p->mbox;
+  a.mbox_pos = p->mbox_next;            // request q posts at mbox_pos + q
   a.bytectr = p->bytectr;
   a.flags = p->flags_dev;
-  a.counter = nullptr;                  // per-request completion replaces the CTA arrival
+  // this launch's own arrival counter: its last CTA resets the counters and
+  // then releases the buffer (requests complete one by one via credits)
+  a.counter = reinterpret_cast<unsigned int*>(B.dev);
+  a.done_word = B.done_dev;
+  a.done_seq = B.seq + 1;
   a.remote_stores = 0;
   a.audit = p->audit_ctr;
   a.src_layer_bytes = sg.layer_bytes;
@@ -1600,25 +1846,17 @@ kvd_status kvd_pull_batch(kvd_peer p, uint32_t num_requests, const uint64_t* req
   uint32_t threads = 0, ctas = 0;
   s = launch_shape(p, pol, a, (uint64_t)n * per_entry, &threads, &ctas);
   if (s != KVD_OK) return s;
-#ifndef KVD_EXPERIMENT_STATIC_TILES
-  if (pol.variant == KVD_VARIANT_TMA && !p->row_bytes) {
-    // dynamic tile claiming; the first request's (otherwise unused) arrival
-    // counter only tells the last CTA to reset the tile counter
-    a.counter = p->counters + slots[0];
-    a.tile_ctr = p->tile_ctrs + slots[0];
-  }
-#endif
+  if (pol.variant == KVD_VARIANT_TMA && !p->row_bytes)
+    a.tile_ctr = reinterpret_cast<unsigned int*>(B.dev) + 1;   // dynamic tile claiming
   timing_begin(p, stream);
   cudaError_t e = kvd::launch_pull(a, p->runs4.data(), pol.variant, ctas, threads, pol.stages, stream);
   timing_end(p, stream);
   if (e != cudaSuccess) return cuda_fail(e, "batched pull launch");
   p->seq += num_requests;
-  for (uint32_t q = 0; q < num_requests; ++q) {
-    p->slot_seq[slots[q]] = tokens[q];
-    p->inflight[request_ids[q]] = kvd_peer_s::InFlight{slots[q], tokens[q], bi};
-  }
-  B.refs = num_requests;
-  p->cursor = (slots.back() + 1) % kSlots;
+  B.seq += 1;
+  if (a.mbox) mbox_commit(p, a.mbox_pos + num_requests);
+  cancel.armed = false;
+  for (uint32_t q = 0; q < num_requests; ++q) slot_publish(p, slots[q], tokens[q], false);
   kvd_pull_info info{};
   info.request_id = request_ids[0];
   info.blocks = n;
@@ -1634,51 +1872,49 @@ kvd_status kvd_pull_batch(kvd_peer p, uint32_t num_requests, const uint64_t* req
   return KVD_OK;
 }
 
+// Lock-free (no peer mutex, no CUDA call): slot lookup, one acquire load of
+// the pinned completion word, and a compare-and-swap to retire.
 kvd_status kvd_poll_done(kvd_peer p, uint64_t request_id, int* done) {
   if (!p || !done) return fail(KVD_EINVAL, "null argument");
-  std::lock_guard<std::mutex> lk(p->mu);
-  auto it = p->inflight.find(request_id);
-  if (it == p->inflight.end())
+  uint32_t i;
+  uint64_t token;
+  if (!slot_find(p, request_id, &i, &token))
     return fail(KVD_EINVAL, "request %llu is not in flight", (unsigned long long)request_id);
-  const uint32_t slot = it->second.slot;
-  const uint64_t token = it->second.token;
-  const uint64_t v = __atomic_load_n(&p->flags[slot], __ATOMIC_ACQUIRE);
-  if (v == token) {
-    *done = 1;
-    p->slot_seq[slot] = 0;
-    if (it->second.timed) {   // written before the slot word's release
-      p->gt_total_ms += (double)__atomic_load_n(&p->gt_host[slot], __ATOMIC_RELAXED) * 1e-6;
-      ++p->gt_count;
-    }
-    if (it->second.batch >= 0) --p->batch_bufs[it->second.batch].refs;
-    p->inflight.erase(it);
-  } else {
-    *done = 0;
-  }
+  *done = 0;
+  if (__atomic_load_n(&p->flags[i], __ATOMIC_ACQUIRE) != token) return KVD_OK;
+  if (!slot_retire(p, i, token))
+    return fail(KVD_EINVAL, "request %llu was retired by a concurrent poll",
+                (unsigned long long)request_id);
+  *done = 1;
   return KVD_OK;
 }
 
+// All or nothing on bad input: every id is looked up (and duplicates
+// rejected) before any request is retired.
 kvd_status kvd_poll_many(kvd_peer p, const uint64_t* request_ids, uint32_t n, uint8_t* done,
                          uint32_t* ndone) {
   if (!p || !ndone || (n && (!request_ids || !done))) return fail(KVD_EINVAL, "null argument");
-  std::lock_guard<std::mutex> lk(p->mu);
+  *ndone = 0;
+  if (n > 1) {
+    std::vector<uint64_t> sorted(request_ids, request_ids + n);
+    std::sort(sorted.begin(), sorted.end());
+    for (uint32_t i = 1; i < n; ++i)
+      if (sorted[i] == sorted[i - 1])
+        return fail(KVD_EINVAL, "request %llu listed twice", (unsigned long long)sorted[i]);
+  }
+  thread_local std::vector<std::pair<uint32_t, uint64_t>> found;
+  found.resize(n);
+  for (uint32_t i = 0; i < n; ++i)
+    if (!slot_find(p, request_ids[i], &found[i].first, &found[i].second))
+      return fail(KVD_EINVAL, "request %llu is not in flight", (unsigned long long)request_ids[i]);
   uint32_t k = 0;
   for (uint32_t i = 0; i < n; ++i) {
-    done[i] = 0;
-    auto it = p->inflight.find(request_ids[i]);
-    if (it == p->inflight.end())
-      return fail(KVD_EINVAL, "request %llu is not in flight", (unsigned long long)request_ids[i]);
-    const uint32_t slot = it->second.slot;
-    if (__atomic_load_n(&p->flags[slot], __ATOMIC_ACQUIRE) != it->second.token) continue;
-    done[i] = 1;
-    ++k;
-    p->slot_seq[slot] = 0;
-    if (it->second.timed) {
-      p->gt_total_ms += (double)__atomic_load_n(&p->gt_host[slot], __ATOMIC_RELAXED) * 1e-6;
-      ++p->gt_count;
-    }
-    if (it->second.batch >= 0) --p->batch_bufs[it->second.batch].refs;
-    p->inflight.erase(it);
+    const uint32_t slot = found[i].first;
+    const uint64_t token = found[i].second;
+    // a concurrent poller that retired it first reports it instead
+    done[i] = __atomic_load_n(&p->flags[slot], __ATOMIC_ACQUIRE) == token &&
+              slot_retire(p, slot, token);
+    k += done[i];
   }
   *ndone = k;
   return KVD_OK;
@@ -1700,40 +1936,44 @@ kvd_status kvd_wait_done(kvd_peer p, uint64_t request_id, int64_t timeout_us) {
   }
 }
 
+// Plain loads of the shared host mailbox: no CUDA call.  Rings are drained
+// in order of ring index, each in position order.
 kvd_status kvd_poll_released(kvd_cache c, uint64_t* request_ids, uint32_t cap, uint32_t* n) {
   if (!c || !n || (cap && !request_ids)) return fail(KVD_EINVAL, "null argument");
   *n = 0;
   std::lock_guard<std::mutex> lk(c->mu);
-  if (!c->mbox_dev) return KVD_OK;               // never exported: nobody can complete
-  DeviceGuard dg(c->device);
-  if (!dg.ok) return fail(KVD_ECUDA, "cannot select device %d", c->device);
-  // a plain cudaMemcpy would run on the legacy default stream and wait for
-  // whatever prefill work the exporter has queued there
-  KVD_CUDA(cudaMemcpyAsync(c->mbox_pinned, c->mbox_dev,
-                           kvd::kMailboxWords * sizeof(unsigned long long),
-                           cudaMemcpyDeviceToHost, c->mbox_stream));
-  KVD_CUDA(cudaStreamSynchronize(c->mbox_stream));
-  const unsigned long long* ring = c->mbox_pinned + 8;
+  if (!c->mbox) return KVD_OK;                   // never exported: nobody can complete
   uint32_t k = 0;
-  while (k < cap) {
-    const uint64_t slot = c->mbox_head % kvd::kReleaseRing;
-    const unsigned long long seq = ring[2 * slot];
-    if (seq == c->mbox_head + 1) {
-      request_ids[k++] = ring[2 * slot + 1];
-      ++c->mbox_head;
-    } else if (seq > c->mbox_head + 1) {
-      // the ring wrapped before this reader caught up: entries were lost
-      const uint64_t lost = seq - (c->mbox_head + 1);
-      c->mbox_head = seq - 1;
-      *n = k;
-      return fail(KVD_EBUSY, "release mailbox overflowed: %llu notifications lost "
-                  "(poll at least every %u completions)", (unsigned long long)lost,
-                  kvd::kReleaseRing);
-    } else {
-      break;                                     // not yet written
+  uint64_t lost = 0;
+  for (uint32_t r = 0; r < kvd::kMailboxRings && k < cap; ++r) {
+    uint64_t& head = c->mbox_head[r];
+    if (__atomic_load_n(mbox_next(c->mbox, r), __ATOMIC_ACQUIRE) == head) continue;   // idle ring
+    const uint64_t* ring = mbox_ring(c->mbox, r);
+    while (k < cap) {
+      const uint64_t* e = ring + 2 * (head % kvd::kReleaseRing);
+      const uint64_t w0 = __atomic_load_n(&e[0], __ATOMIC_ACQUIRE);
+      const uint64_t w1 = __atomic_load_n(&e[1], __ATOMIC_ACQUIRE);
+      const uint32_t want = (uint32_t)(head + 1);
+      const int32_t d0 = (int32_t)((uint32_t)(w0 >> 32) - want);
+      const int32_t d1 = (int32_t)((uint32_t)(w1 >> 32) - want);
+      if (d0 == 0 && d1 == 0) {
+        request_ids[k++] = (w0 & 0xffffffffull) | (w1 << 32);
+        ++head;
+      } else if (d0 > 0 || d1 > 0) {
+        // the ring wrapped before this reader caught up: entries were lost
+        const int32_t d = std::max(d0, d1);
+        lost += (uint64_t)d;
+        head += (uint64_t)d;
+      } else {
+        break;                                   // not yet written
+      }
     }
   }
   *n = k;
+  if (lost)
+    return fail(KVD_EBUSY, "release mailbox overflowed: %llu notifications lost "
+                "(poll at least every %u completions per importer)", (unsigned long long)lost,
+                kvd::kReleaseRing);
   return KVD_OK;
 }
 
@@ -1785,11 +2025,8 @@ kvd_status kvd_stream_wait(kvd_peer p, void* stream) {
 
 kvd_status kvd_peer_device_time(kvd_peer p, double* total_ms, uint64_t* launches) {
   if (!p || !total_ms || !launches) return fail(KVD_EINVAL, "null argument");
-  std::lock_guard<std::mutex> lk(p->mu);
-  *total_ms = p->gt_total_ms;
-  *launches = p->gt_count;
-  p->gt_total_ms = 0;
-  p->gt_count = 0;
+  *total_ms = (double)p->gt_ns.exchange(0, std::memory_order_relaxed) * 1e-6;
+  *launches = p->gt_count.exchange(0, std::memory_order_relaxed);
   return KVD_OK;
 }
 

@@ -8,11 +8,23 @@
 namespace kvd {
 
 // Release mailbox (Complete() -> prefill, "sends the request ID to the
-// prefill worker"): device memory owned by the EXPORTER, IPC-mapped by every
-// importer.  u64 words: [0] tail (claimed with a system-scope atomic), [1..7]
-// padding, then kReleaseRing entries of {seq = slot + 1, request_id}.
+// prefill worker"): pinned HOST memory owned by the EXPORTER (a memfd the
+// importers map and register with cudaHostRegister), so the prefill host
+// reads completions with plain loads -- no CUDA call, no NVLink atomic.
+// u64 words: a header of kMailboxHeaderWords (magic, rings, entries, then
+// per ring an owner word and a next-position word), then kMailboxRings
+// single-producer rings of kReleaseRing entries.  An importer claims one
+// ring at open (CPU compare-and-swap on its owner word) and assigns each
+// request a position p in issue order; the completing CTA writes entry
+// p % kReleaseRing as two 64-bit words {tag | id_lo32, tag | id_hi32} with
+// tag = low32(p + 1) << 32 (each word is single-copy atomic, so the reader
+// accepts an entry once both words carry the expected tag; no fence and no
+// read-modify-write over the link).
 constexpr unsigned int kReleaseRing = 4096;
-constexpr size_t kMailboxWords = 8 + 2 * (size_t)kReleaseRing;
+constexpr unsigned int kMailboxRings = 64;
+constexpr size_t kMailboxHeaderWords = 8 + 2 * (size_t)kMailboxRings;
+constexpr size_t kMailboxWords = kMailboxHeaderWords + 2 * (size_t)kReleaseRing * kMailboxRings;
+constexpr unsigned long long kMailboxMagic = 0x584f42444b56444bull;   // "KDVKDBOX"
 
 // Where layer l of one side starts: table ? table[l] : base + l * step.
 // The peer's source side uses a device table of IPC-mapped prefill layer
@@ -47,7 +59,9 @@ struct PullArgs {
   unsigned long long* flag;         // per-slot completion word (pinned, host-mapped)
   unsigned long long token;         // value stored to *flag when every byte has landed
   unsigned long long request_id;    // posted to the exporter's release mailbox (if any)
-  unsigned long long* mbox;         // exporter's mailbox, mapped here (nullptr: none)
+  unsigned long long* mbox;         // this importer's ring of the exporter's mailbox, mapped
+                                    // here (device pointer to host memory; nullptr: none)
+  unsigned long long mbox_pos;      // ring position of this request (batches: of request 0)
   const int4* runs_dev;             // run table in device memory when nruns > params capacity
   unsigned int remote_stores;       // 1: stores target a peer GPU (push) -> system-scope fences
   unsigned int tiles_per_warp;      // LSU chunk = warps * this (host sets it; grid follows)
@@ -68,6 +82,18 @@ struct PullArgs {
   // which pipes claim tiles dynamically; reset by the last CTA.  nullptr:
   // static grid-stride order.
   unsigned int* tile_ctr;
+  // TMA single pulls over NVLink: lane 0 of each pipe claims and issues its
+  // first ring of bulk loads from the SOURCE before griddepcontrol.wait, so
+  // the ramp of a pull overlaps the drain and completion tail of the pull
+  // before it on the stream.  Only the source (the prefill's finished cache)
+  // is read early; every store into the decode cache waits.
+  unsigned int early_loads;
+  // Batches: the launch's own arrival/tile counters live with its
+  // descriptor buffer; the last CTA resets them and then releases done_seq
+  // into *done_word (pinned, host-mapped), after which the host may reuse
+  // the buffer and its counters.
+  unsigned long long* done_word;
+  unsigned long long done_seq;
 
   // TP-resharding (§8 f4): row_bytes > 0 makes every unit block_size rows
   // of row_bytes, src_row_stride / dst_row_stride apart, and shifts the
@@ -113,10 +139,11 @@ cudaError_t launch_pull(const PullArgs& args, const int4* runs_host, int variant
                         cudaStream_t stream);
 
 // Completion with no bytes (n = 0, or after copy-engine copies); also posts
-// request_id to the exporter's release mailbox when mbox is non-null.
+// request_id at ring position mbox_pos of the exporter's release mailbox when
+// mbox is non-null.
 cudaError_t launch_flag_only(unsigned long long* flag, unsigned long long token,
-                             unsigned long long* mbox, unsigned long long request_id,
-                             cudaStream_t stream);
+                             unsigned long long* mbox, unsigned long long mbox_pos,
+                             unsigned long long request_id, cudaStream_t stream);
 
 // Resident CTAs per SM of the pull kernel for the given threads per CTA.
 int pull_ctas_per_sm(int variant, unsigned int threads, unsigned int nruns);

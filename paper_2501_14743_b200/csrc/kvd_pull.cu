@@ -114,10 +114,10 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 // touches any global memory (pdl_wait) -- stream order is unchanged, only the
 // launch latency overlaps the tail.  After a non-PDL kernel both are no-ops.
 __device__ __forceinline__ void pdl_wait() {
-#ifndef KVD_EXPERIMENT_NO_PDL_WAIT   // A/B only: checks the ordering test can fail
   asm volatile("griddepcontrol.wait;" ::: "memory");
-#endif
 }
+// The first thread of a CTA to execute it triggers the CTA (later executions
+// by any thread of the CTA have no further effect).
 __device__ __forceinline__ void pdl_trigger() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
@@ -285,36 +285,30 @@ __device__ __forceinline__ bool tile_in_bounds(const PullArgs& a, const Tile& T,
 
 // Complete() to the prefill side ("The completion transaction sends
 // the request ID to the prefill worker"; it then releases the
-// blocks): claim a slot of the exporter's mailbox with a system-scope atomic
-// over NVLink, write the id, then release the slot's sequence word (the
-// release orders the id store before it).  Called after every byte of the
-// request has landed, i.e. after its last remote read.  Split in two so the
-// claim's NVLink round trip (~1.5 us) overlaps the host-flag release that
-// sits between them (fence_probe: 4.5 -> 3.1 us for the whole sequence).
-__device__ __forceinline__ unsigned long long mbox_claim(const PullArgs& a) {
-#ifdef KVD_EXPERIMENT_NO_MBOX   // A/B experiment only: no prefill notification
-  return 0ull;
-#endif
-  return a.mbox ? atomicAdd_system(a.mbox, 1ull) : 0ull;
-}
-__device__ __forceinline__ void mbox_post(const PullArgs& a, unsigned long long s,
+// blocks).  The exporter's mailbox is host memory shared with this process;
+// this importer owns one single-producer ring of it and the host assigned
+// the request its position, so the post is two plain 64-bit stores (each
+// single-copy atomic, both tagged with the position), posted over PCIe: no
+// atomic round trip over NVLink and no second system-scope fence.  It is
+// issued after the slot word's release, i.e. after every byte of the
+// request landed -- and so after every read of the prefill's blocks.
+__device__ __forceinline__ void mbox_post(const PullArgs& a, unsigned long long pos,
                                           unsigned long long request_id) {
   if (a.mbox == nullptr) return;
-#ifdef KVD_EXPERIMENT_NO_MBOX
-  return;
-#endif
-  unsigned long long* e = a.mbox + 8 + 2 * (s % kReleaseRing);
-  *(volatile unsigned long long*)(e + 1) = request_id;
-  st_release_sys(e, s + 1);
+  unsigned long long* e = a.mbox + 2 * (pos % kReleaseRing);
+  const unsigned long long tag = (unsigned long long)(unsigned int)(pos + 1) << 32;
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" :: "l"(e), "l"(tag | (request_id & 0xffffffffull)) : "memory");
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" :: "l"(e + 1), "l"(tag | (request_id >> 32)) : "memory");
 }
-// Publish a finished request: claim the mailbox slot, release the token into
-// the host-visible slot word, then post the id to the exporter.
+// Publish a finished request: release the token into the host-visible slot
+// word (one system-scope release orders every byte before it), then post the
+// id to the exporter.
 __device__ __forceinline__ void publish_token(const PullArgs& a, unsigned long long* flag,
                                               unsigned long long token,
-                                              unsigned long long request_id) {
-  const unsigned long long s = mbox_claim(a);
+                                              unsigned long long request_id,
+                                              unsigned long long pos) {
   st_release_sys(flag, token);
-  mbox_post(a, s, request_id);
+  mbox_post(a, pos, request_id);
 }
 
 // --- batched drain (f1): per-request completion inside one launch ----------
@@ -325,14 +319,7 @@ __device__ __forceinline__ void publish(const PullArgs& a, unsigned int q) {
   const uint4 R = a.reqs[q];
   a.bytectr[R.y] = 0ull;                 // slot idle again
   fence_acq_rel_gpu();
-#if defined(KVD_EXPERIMENT_PUBLISH_GPU_SCOPE)   // A/B experiment only: unsound for the host
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" :: "l"(&a.flags[R.y]), "l"(a.tokens[q]) : "memory");
-  return;
-#elif defined(KVD_EXPERIMENT_PUBLISH_NO_MBOX)   // A/B experiment only: no prefill notification
-  st_release_sys(&a.flags[R.y], a.tokens[q]);
-  return;
-#endif
-  publish_token(a, &a.flags[R.y], a.tokens[q], a.req_ids[q]);
+  publish_token(a, &a.flags[R.y], a.tokens[q], a.req_ids[q], a.mbox_pos + q);
 }
 
 // Credit `bytes` landed bytes to request q; the credit that reaches the
@@ -345,9 +332,6 @@ __device__ __forceinline__ void credit(const PullArgs& a, unsigned int q, unsign
 }
 
 __device__ __forceinline__ void fence_stores(const PullArgs& a) {
-#ifdef KVD_EXPERIMENT_NO_CREDIT_FENCE   // A/B experiment only: unsound ordering
-  return;
-#endif
   if (a.remote_stores) __threadfence_system(); else __threadfence();
 }
 
@@ -417,6 +401,8 @@ __device__ __forceinline__ void publish_empty(const PullArgs& a) {
 // this GPU), resets the slot counter and publishes the token with ONE
 // system-scope release, so a host acquire load of the word implies every
 // byte landed; the prefill-side notification follows (publish_token).
+// Batches published their requests one by one; their last CTA only resets
+// the launch's counters and releases the descriptor buffer to the host.
 __device__ __forceinline__ void complete(const PullArgs& a) {
   if (a.counter == nullptr) return;   // baseline gather/scatter: stream order only
   if (a.remote_stores) __threadfence_system(); else __threadfence();
@@ -427,13 +413,16 @@ __device__ __forceinline__ void complete(const PullArgs& a) {
       *a.counter = 0u;
       fence_acq_rel_gpu();
       if (a.tile_ctr != nullptr) *a.tile_ctr = 0u;   // every claim happened before its CTA arrived
-      if (a.nreqs) return;           // batches: requests completed one by one (publish)
+      if (a.nreqs) {                 // batches: requests completed one by one (publish)
+        if (a.done_word != nullptr) st_release_sys(a.done_word, a.done_seq);
+        return;
+      }
       if (a.gt_start != nullptr) {   // first CTA start -> last CTA done, before the release
         const unsigned long long t1 = globaltimer();
         *(volatile unsigned long long*)a.gt_out = t1 - *(volatile unsigned long long*)a.gt_start;
         *a.gt_start = ~0ull;
       }
-      publish_token(a, a.flag, a.token, a.request_id);
+      publish_token(a, a.flag, a.token, a.request_id, a.mbox_pos);
     }
   }
 }
@@ -557,7 +546,13 @@ pull_kernel_tma(const __grid_constant__ PullParams<MAXR> P, unsigned int stages)
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint64_t bars[(256 / 32) * kMaxStages];   // <= 8 pipes (launch bound)
   const PullArgs& a = P.a;
-  pdl_wait();
+  // early_loads: only lane 0 of each pipe touches global memory before the
+  // kernel ends (claims, bulk loads, bulk stores), and it waits for the
+  // preceding grid right before its first store; everything before that
+  // reads the kernel parameters, the layer-base tables (written once at
+  // open), this launch's tile counter and the SOURCE blocks.
+  const bool early = a.early_loads != 0;
+  if (!early) pdl_wait();
   mark_start(a);
   const unsigned int warp = threadIdx.x >> 5;
   const unsigned int pipes_per_cta = blockDim.x >> 5;
@@ -614,13 +609,39 @@ pull_kernel_tma(const __grid_constant__ PullParams<MAXR> P, unsigned int stages)
     Tile pend[kCreditLag + 1];
     Credit cr;
     unsigned int issued = 0;                 // tiles loaded into the ring so far
-    for (unsigned int k = 0; k < S; ++k) {
+    // Programmatic dependent launch: this pipe lets the next pull on the
+    // stream launch as soon as it has claimed its last tile (its ring still
+    // drains S tiles), so with early loads the next pull's first ring is in
+    // flight over the link while this one drains and completes.  Never
+    // before this pipe's own wait returned: at most two pulls (one draining,
+    // one ramping) hold SMs at a time.
+    bool triggered = false, waited = !early, exhausted = false;
+    auto claim = [&]() -> unsigned int {
       const unsigned int t = next();
+      if (t == kNone) {
+        exhausted = true;
+        if (waited && !triggered) {
+          pdl_trigger();
+          triggered = true;
+        }
+      }
+      return t;
+    };
+    for (unsigned int k = 0; k < S; ++k) {
+      const unsigned int t = claim();
       if (t == kNone) break;
       tiles[k] = audited(a, tile_at(a, runs, t), t);
       tma_load(ring + (size_t)k * a.tile_bytes, tiles[k].src, tiles[k].skip ? 0u : tiles[k].bytes,
                &bar[k]);
       ++issued;
+    }
+    if (early) {                             // stores below: the preceding grid is done
+      pdl_wait();
+      waited = true;
+      if (exhausted && !triggered) {
+        pdl_trigger();
+        triggered = true;
+      }
     }
     for (unsigned int i = 0; i < issued; ++i) {
       const unsigned int s = i % S;
@@ -633,7 +654,7 @@ pull_kernel_tma(const __grid_constant__ PullParams<MAXR> P, unsigned int stages)
         // refill the stage of tile i-1 with the ring's tile number i-1+S
         // (only while no claim has failed: tile j always lives in stage j % S)
         if (issued == i - 1 + S) {
-          const unsigned int t = next();
+          const unsigned int t = claim();
           if (t != kNone) {
             tiles[sp] = audited(a, tile_at(a, runs, t), t);
             tma_load(ring + (size_t)sp * a.tile_bytes, tiles[sp].src,
@@ -745,11 +766,12 @@ pull_kernel_tma_rows(const __grid_constant__ PullParams<MAXR> P, unsigned int st
 }
 
 __global__ void flag_kernel(unsigned long long* flag, unsigned long long token,
-                            unsigned long long* mbox, unsigned long long request_id) {
+                            unsigned long long* mbox, unsigned long long mbox_pos,
+                            unsigned long long request_id) {
   // no data: earlier stream work is ordered by the stream itself
   PullArgs a{};
   a.mbox = mbox;
-  publish_token(a, flag, token, request_id);
+  publish_token(a, flag, token, request_id, mbox_pos);
 }
 
 // ---------------------------------------------------------------------------
@@ -780,11 +802,7 @@ cudaError_t launch_pdl(Kernel kernel, unsigned int ctas, unsigned int threads, s
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-#ifdef KVD_EXPERIMENT_NO_PDL
-  cfg.numAttrs = 0;
-#else
   cfg.numAttrs = 1;
-#endif
   return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
@@ -888,9 +906,9 @@ cudaError_t launch_pull(const PullArgs& args, const int4* runs_host, int variant
 }
 
 cudaError_t launch_flag_only(unsigned long long* flag, unsigned long long token,
-                             unsigned long long* mbox, unsigned long long request_id,
-                             cudaStream_t stream) {
-  flag_kernel<<<1, 1, 0, stream>>>(flag, token, mbox, request_id);
+                             unsigned long long* mbox, unsigned long long mbox_pos,
+                             unsigned long long request_id, cudaStream_t stream) {
+  flag_kernel<<<1, 1, 0, stream>>>(flag, token, mbox, mbox_pos, request_id);
   return cudaGetLastError();
 }
 

@@ -22,7 +22,7 @@ FP16, BF16, FP8, FP32 = 0, 1, 2, 3
 VARIANT_AUTO, VARIANT_LSU, VARIANT_LSU32, VARIANT_CE, VARIANT_TMA = 0, 1, 2, 3, 4
 MEM_AUTO, MEM_POSIX_FD, MEM_FABRIC = 0, 1, 8
 OPT_MAX_CTAS, OPT_TILE_BYTES, OPT_COALESCE, OPT_VARIANT, OPT_THREADS, OPT_STAGES = 0, 1, 2, 3, 4, 5
-OPT_AUDIT, OPT_TIMING, OPT_STREAMS = 6, 7, 8
+OPT_AUDIT, OPT_TIMING, OPT_STREAMS, OPT_EARLY_LOADS = 6, 7, 8, 9
 
 EXPORTED = (
     "kvd_layout_geometry", "kvd_plan", "kvd_blob_info", "kvd_register_cache",
@@ -80,6 +80,15 @@ if not os.path.exists(LIB_PATH):
 
 _lib = ctypes.CDLL(LIB_PATH)
 
+# The ABI version is checked before any other symbol is bound, so a stale
+# library fails here with a clear message rather than with AttributeError.
+ABI_VERSION = 2     # include/kvd.h KVD_ABI_VERSION this binding was written against
+_lib.kvd_abi_version.argtypes = []
+_lib.kvd_abi_version.restype = ctypes.c_int
+if _lib.kvd_abi_version() != ABI_VERSION:
+    raise ImportError(f"{LIB_PATH} has ABI {_lib.kvd_abi_version()}, the binding expects "
+                      f"{ABI_VERSION}: rebuild it (__graft_entry__.build())")
+
 _p = ctypes.c_void_p
 _u32, _u64, _i32, _i64 = ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int32, ctypes.c_int64
 _pi32 = ctypes.POINTER(ctypes.c_int32)
@@ -125,12 +134,6 @@ _lib.kvd_strerror.argtypes = [ctypes.c_int]
 _lib.kvd_strerror.restype = ctypes.c_char_p
 _lib.kvd_last_error.argtypes = []
 _lib.kvd_last_error.restype = ctypes.c_char_p
-_lib.kvd_abi_version.argtypes = []
-_lib.kvd_abi_version.restype = ctypes.c_int
-ABI_VERSION = 1     # include/kvd.h KVD_ABI_VERSION this binding was written against
-if _lib.kvd_abi_version() != ABI_VERSION:
-    raise ImportError(f"{LIB_PATH} has ABI {_lib.kvd_abi_version()}, the binding expects "
-                      f"{ABI_VERSION}: rebuild it (__graft_entry__.build())")
 
 
 def _check(status: int, where: str) -> int:
@@ -322,7 +325,9 @@ def kvd_poll_done(peer: int, request_id: int) -> bool:
 
 
 def kvd_poll_many(peer: int, request_ids) -> list:
-    """Retire every completed request among `request_ids`; returns those ids."""
+    """Retire every completed request among `request_ids`; returns those ids.
+    All or nothing: an id not in flight (or listed twice) raises KvdError
+    before any request is retired."""
     ids = np.ascontiguousarray(np.asarray(request_ids, dtype=np.uint64).reshape(-1))
     done = np.zeros(max(1, ids.size), dtype=np.uint8)
     n = _u32(0)

@@ -15,11 +15,12 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 MAGIC = 0x4244564B
 
 
-def make_blob(device, pid, layers=3, allocs=2, num_blocks=64, kinds=None):
-    """A blob in the wire format of kvd_export_handle, v3 (test-side encoder).
-    kinds: per-allocation handle kind (0 legacy IPC, 1 POSIX fd, 8 fabric)."""
+def make_blob(device, pid, layers=3, allocs=2, num_blocks=64, kinds=None, mailbox=False):
+    """A blob in the wire format of kvd_export_handle, v4 (test-side encoder).
+    kinds: per-allocation handle kind (0 legacy IPC, 1 POSIX fd, 8 fabric);
+    mailbox: append the release-mailbox record (memfd number, bytes)."""
     kinds = kinds or [0] * allocs
-    b = struct.pack("<IIII", MAGIC, 3, device, 0)
+    b = struct.pack("<IIII", MAGIC, 4, device, 0)
     b += struct.pack("<QQ", pid, 0xABCDEF)
     b += struct.pack("<IIIIII", layers, 2, 64, 16, num_blocks, 0)   # layers, heads, dim, bs, nb, fp16
     sub = 16 * 2 * 64
@@ -32,7 +33,10 @@ def make_blob(device, pid, layers=3, allocs=2, num_blocks=64, kinds=None):
                                                layers * layer_bytes)
     for l in range(layers):
         b += struct.pack("<IIQ", l % allocs, 0, (l // allocs) * layer_bytes)
-    b += struct.pack("<I", 0)              # no release mailbox
+    if mailbox:
+        b += struct.pack("<IIIQ", 1, 9, 0, 4 << 20)
+    else:
+        b += struct.pack("<I", 0)          # no release mailbox
     b += struct.pack("<I", MAGIC)
     return b
 
@@ -129,7 +133,7 @@ def test_synthesised_blob_round_trip_and_corruption():
 
 
 def test_blob_handle_kinds():
-    """Blob v3 records a handle kind per allocation (legacy IPC, POSIX fd,
+    """The blob records a handle kind per allocation (legacy IPC, POSIX fd,
     fabric -- §8 f3 groundwork); unknown kinds and older versions are refused."""
     from paper_2501_14743_b200 import kvd
     for kinds in ([0, 0], [1, 1], [8, 0], [1, 8]):
@@ -142,3 +146,24 @@ def test_blob_handle_kinds():
     old[4:8] = struct.pack("<I", 2)
     with pytest.raises(kvd.KvdError):
         kvd.kvd_blob_info(bytes(old))
+
+
+def test_blob_v4_mailbox_record():
+    """Blob v4 carries the release mailbox as (memfd number, bytes) of the
+    exporter's host memory; a truncated record, a bad flag or a v3 blob are
+    refused."""
+    from paper_2501_14743_b200 import kvd
+    blob = make_blob(1, 77, mailbox=True)
+    layout, dev, pid, na = kvd.kvd_blob_info(blob)
+    assert (dev, pid, na) == (1, 77, 2)
+    cut = blob[:-4 - 8] + blob[-4:]                   # mailbox record missing its size
+    with pytest.raises(kvd.KvdError):
+        kvd.kvd_blob_info(cut)
+    bad = bytearray(blob)
+    bad[-4 - 20:-4 - 16] = struct.pack("<I", 2)       # mailbox flag must be 0 or 1
+    with pytest.raises(kvd.KvdError):
+        kvd.kvd_blob_info(bytes(bad))
+    v3 = bytearray(blob)
+    v3[4:8] = struct.pack("<I", 3)
+    with pytest.raises(kvd.KvdError):
+        kvd.kvd_blob_info(bytes(v3))

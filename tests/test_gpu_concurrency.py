@@ -171,3 +171,143 @@ def test_poll_many_retires_completed_requests():
         assert_layers_equal(pair.download_dst(), exp)
     finally:
         pair.close()
+
+
+def test_poll_many_bad_input_changes_nothing():
+    """All or nothing (kvd_poll_many): a duplicate or unknown id is refused
+    before any request is retired, so completions are never lost."""
+    from paper_2501_14743_b200 import kvd
+    pair = make_pair(G, G, seed=75)
+    try:
+        tables = kvdgen.disjoint_fragmented_tables([20, 25, 30], 512, 512, seed=10)
+        rids = []
+        for s, d in tables:
+            rid = next_request_id()
+            pair.peer.pull(rid, s, d)
+            rids.append(rid)
+        torch.cuda.synchronize()                        # all three have completed
+        for bad in (rids + [rids[1]], rids + [next_request_id() + 10**9]):
+            with pytest.raises(kvd.KvdError) as ei:
+                pair.peer.poll_many(bad)
+            assert ei.value.status == kvd.EINVAL
+        # nothing was retired by the failed calls: every id still reports once
+        assert sorted(pair.peer.poll_many(rids)) == sorted(rids)
+        exp = pair.dst_host
+        for s, d in tables:
+            exp = pair.expected(s, d, exp)
+        assert_layers_equal(pair.download_dst(), exp)
+    finally:
+        pair.close()
+
+
+def test_poll_does_not_wait_for_a_concurrent_launch():
+    """kvd_poll_done is lock-free (SURVEY §8 b threading): a
+    thread polling an in-flight request of a peer while another thread
+    issues host-heavy kvd_pulls on the SAME peer (60k uncoalesced blocks
+    each: validation, planning, a run-table upload and the launch) sees a
+    poll latency that does not track the kvd_pull call time."""
+    import time
+    from paper_2501_14743_b200 import kvd
+    g = kvdgen.CacheGeom(1, 1, 64, 16, 65536, kvdgen.FP16)   # 2 KiB spans, 64k blocks
+    pair = make_pair(g, g, seed=76)
+    try:
+        pair.peer.set(kvd.OPT_COALESCE, 0)
+        rng = np.random.default_rng(0)
+        n = 60000
+        stop = threading.Event()
+        polls = []
+        target = [None]
+
+        def poller():
+            while not stop.is_set():
+                rid = target[0]
+                if rid is None:
+                    continue
+                t0 = time.perf_counter_ns()
+                try:
+                    done = pair.peer.poll(rid)
+                except kvd.KvdError:
+                    done = True
+                dt = time.perf_counter_ns() - t0
+                if not done:
+                    polls.append(dt)
+
+        th = threading.Thread(target=poller)
+        th.start()
+        pulls = []
+        side = torch.cuda.Stream()
+        try:
+            for it in range(6):
+                # `target` stays in flight behind a ~20 ms sleep on its stream
+                rid = next_request_id()
+                with torch.cuda.stream(side):
+                    torch.cuda._sleep(40_000_000)
+                pair.peer.pull(rid, [65535 - it], [65535 - it], side)
+                target[0] = rid
+                for _ in range(3):
+                    s = rng.choice(65000, n, replace=False).astype(np.int32)
+                    d = rng.choice(65000, n, replace=False).astype(np.int32)
+                    r = next_request_id()
+                    t0 = time.perf_counter_ns()
+                    pair.peer.pull(r, s, d)
+                    pulls.append(time.perf_counter_ns() - t0)
+                    pair.peer.wait(r)
+                target[0] = None
+                side.synchronize()
+                try:
+                    pair.peer.wait(rid)
+                except kvd.KvdError:
+                    pass                                   # the poller retired it
+        finally:
+            stop.set()
+            th.join()
+        pull_med = float(np.median(pulls))
+        assert len(polls) > 100, len(polls)
+        p90 = float(np.percentile(polls, 90))
+        print(f"kvd_pull median {pull_med / 1e3:.1f} us; poll p50 "
+              f"{np.median(polls) / 1e3:.2f} us p90 {p90 / 1e3:.2f} us over {len(polls)} polls")
+        assert p90 < 0.25 * pull_med, (p90, pull_med)
+    finally:
+        pair.close()
+
+
+def test_batch_slot_reuse_while_batch_runs():
+    """a TMA batch's counters belong to its descriptor buffer, not
+    to request 0's completion slot.  Request 0 completes first; its id (hence
+    its slot) is reused by a pull on a second stream while the batch is still
+    moving its big requests; both stay bit-exact."""
+    from paper_2501_14743_b200 import kvd
+    g = kvdgen.CacheGeom(8, 8, 128, 16, 2048, kvdgen.BF16)    # 32 KiB spans
+    pair = make_pair(g, g, seed=77)
+    try:
+        pair.peer.set(kvd.OPT_VARIANT, kvd.VARIANT_TMA)
+        tables = kvdgen.disjoint_fragmented_tables([1, 600, 600, 600, 40], 2048, 2048, seed=11)
+        ids = [next_request_id() for _ in range(4)]
+        pair.peer.pull_batch(ids, tables[:4])
+        while not pair.peer.poll(ids[0]):
+            pass
+        still = [i for i in ids[1:] if not pair.peer.poll(i)]
+        other = torch.cuda.Stream()
+        s, d = tables[4]
+        pair.peer.pull(ids[0], s, d, other)     # same id -> request 0's slot
+        pair.peer.wait(ids[0])
+        for i in still:
+            pair.peer.wait(i)
+        print(f"{len(still)} batch requests were still in flight at the reuse")
+        exp = pair.dst_host
+        for s, d in tables:
+            exp = pair.expected(s, d, exp)
+        assert_layers_equal(pair.download_dst(), exp)
+        # the batch buffer is reused by the next batch once its kernel ended
+        ids2 = [next_request_id() for _ in range(2)]
+        t2 = kvdgen.disjoint_fragmented_tables([50, 50], 2048, 2048, seed=12)
+        pre = pair.download_dst()
+        pair.peer.pull_batch(ids2, t2)
+        for i in ids2:
+            pair.peer.wait(i)
+        exp = pre
+        for s, d in t2:
+            exp = pair.expected(s, d, exp)
+        assert_layers_equal(pair.download_dst(), exp)
+    finally:
+        pair.close()

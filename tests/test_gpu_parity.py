@@ -267,12 +267,14 @@ def test_completion_flag_never_precedes_data():
 
 @pytest.mark.parametrize("single_allocation,devs", [(False, (0, 0)), (True, (0, 0)),
                                                     (False, (0, 1))])
-def test_c2_full_size_sampled(single_allocation, devs):
-    """C2 at full size (32 layers x 32 heads x 128, 8K tokens = 4 GiB) in the
-    launch configurations bench.py times (N = 1 loopback: LSU; N >= 2 over
-    NVLink: the auto TMA ring); checked on sampled elements against the
-    oracle's element addresses, plus a whole-request property check (every
-    pulled block equals its source block) on the device."""
+def test_c2_full_size_vs_oracle(single_allocation, devs):
+    """C2 at full size (32 layers x 32 heads x 128, 8K tokens = 4 GiB out of
+    8 GiB pools) in the launch configuration bench.py times (N = 1 loopback:
+    LSU32; N >= 2 over NVLink: the auto TMA ring), compared element by element
+    with the CPU oracle: every byte of every layer of the decode cache --
+    pulled blocks and untouched ones -- equals the oracle's result on host
+    copies of the same inputs (layers split over host threads)."""
+    from concurrent.futures import ThreadPoolExecutor
     from gpu_helpers import cache_for
     from oracle import oracle
     if max(devs) >= torch.cuda.device_count():
@@ -281,44 +283,39 @@ def test_c2_full_size_sampled(single_allocation, devs):
     n = kvdgen.blocks_for(kvdgen.C2_TOKENS, g.block_size)
     src = cache_for(g, devs[0], single_allocation)
     dst = cache_for(g, devs[1], single_allocation)
-    ddev = torch.device("cuda", devs[1])
     for l in range(g.num_layers):
         kvdgen.torch_fill_random_(src.layers[l], 1000 + l)
         kvdgen.torch_fill_random_(dst.layers[l], 2000 + l)
+    torch.cuda.synchronize(devs[0])
+    torch.cuda.synchronize(devs[1])
+    # the oracle's inputs: host copies of exactly what the kernel reads / overwrites
+    src_host = [t.cpu().numpy() for t in src.layers]
+    pre_host = [t.cpu().numpy() for t in dst.layers]
     peer = dst.open_peer(src.export())
     try:
         s_ids, d_ids = kvdgen.fragmented_table(n, g.num_blocks, g.num_blocks, seed=1)
-        rng = np.random.default_rng(5)
-        untouched = np.setdiff1d(np.arange(g.num_blocks), d_ids)[:16]
-        span = src.span_bytes
-        before = {l: dst.layers[l].view(2, g.num_blocks, span)[:, torch.from_numpy(untouched).long().to(ddev)].cpu()
-                  for l in (0, g.num_layers - 1)}
         rid = next_request_id()
         peer.pull(rid, s_ids, d_ids)
         peer.wait(rid)
         info = peer.info()
         assert info["bytes"] == 4 * 2**30
         assert info["variant"] == (4 if devs[0] != devs[1] else 2)   # the bench's movers
-        # sampled elements, addresses from the oracle's dot product
-        e = g.elem_bytes
-        for _ in range(2000):
-            l = int(rng.integers(g.num_layers)); i = int(rng.integers(n))
-            kv, t, h, d = (int(rng.integers(2)), int(rng.integers(16)), int(rng.integers(32)),
-                           int(rng.integers(128)))
-            so = oracle.c_layer_element_offset((0,) * 5, g.num_blocks, 16, 32, 128, e,
-                                               int(s_ids[i]), kv, t, h, d)
-            do = oracle.c_layer_element_offset((0,) * 5, g.num_blocks, 16, 32, 128, e,
-                                               int(d_ids[i]), kv, t, h, d)
-            assert torch.equal(dst.layers[l][do:do + e].cpu(), src.layers[l][so:so + e].cpu())
-        # whole request on device + untouched blocks
-        si = torch.from_numpy(s_ids).long().to(src.layers[0].device)
-        di = torch.from_numpy(d_ids).long().to(ddev)
-        for l in range(g.num_layers):
-            assert torch.equal(dst.layers[l].view(2, g.num_blocks, span)[:, di],
-                               src.layers[l].view(2, g.num_blocks, span)[:, si].to(ddev)), l
-        for l, b in before.items():
-            now = dst.layers[l].view(2, g.num_blocks, span)[:, torch.from_numpy(untouched).long().to(ddev)].cpu()
-            assert torch.equal(now, b)
+        torch.cuda.synchronize(devs[1])
+
+        def layer(l):
+            exp = [pre_host[l]]
+            rc = oracle.pull([src_host[l]], g.stride, g.num_blocks, exp, g.stride, g.num_blocks,
+                             g.num_kv_heads, g.head_dim, g.block_size, g.elem_bytes, s_ids, d_ids)
+            assert rc == oracle.OK
+            got = dst.layers[l].cpu().numpy()
+            if not np.array_equal(got, exp[0]):
+                bad = np.flatnonzero(got != exp[0])
+                return f"layer {l}: {bad.size} bytes differ, first at {bad[0]}"
+            return None
+
+        with ThreadPoolExecutor(8) as ex:
+            errs = [e for e in ex.map(layer, range(g.num_layers)) if e]
+        assert not errs, errs[:4]
     finally:
         peer.close()
         dst.close()

@@ -124,3 +124,49 @@ def test_poll_released_does_not_wait_for_exporter_work():
         assert dt < 0.3, f"poll_released waited {dt:.3f} s behind the default stream"
     finally:
         pair.close()
+
+
+def test_release_rings_per_importer():
+    """The mailbox is host memory shared by the exporter and its importers;
+    each open peer owns one single-producer ring (64 at a time).  Two
+    importers' releases both reach the exporter; a closed importer's ring is
+    reused by the next one, which continues its positions; a 65th importer
+    is refused with KVD_EBUSY."""
+    from gpu_helpers import cache_for
+    pair = make_pair(G, G, seed=65)
+    extra = []
+    try:
+        other = cache_for(G, 0)
+        extra.append(other)
+        p2 = other.open_peer(pair.src.export())
+        ids1, ids2 = [], []
+        for k in range(5):
+            s, d = kvdgen.random_table(9, 256, 256, seed=40 + k)
+            r1, r2 = next_request_id(), next_request_id()
+            pair.peer.pull(r1, s, d)
+            p2.pull(r2, s, d)
+            ids1.append(r1)
+            ids2.append(r2)
+        for r in ids1:
+            pair.peer.wait(r)
+        for r in ids2:
+            p2.wait(r)
+        assert sorted(pair.src.poll_released()) == sorted(ids1 + ids2)
+        p2.close()
+        p3 = other.open_peer(pair.src.export())           # takes the freed ring
+        r3 = next_request_id()
+        p3.pull(r3, [5], [6])
+        p3.wait(r3)
+        assert pair.src.poll_released() == [r3]
+        peers = [p3]
+        with pytest.raises(kvd.KvdError) as ei:
+            for _ in range(70):
+                peers.append(other.open_peer(pair.src.export()))
+        assert ei.value.status == kvd.EBUSY
+        assert len(peers) == 63                           # + pair.peer = 64 rings
+        for p in peers:
+            p.close()
+    finally:
+        pair.close()
+        for c in extra:
+            c.close()

@@ -55,6 +55,9 @@ def main():
     ap.add_argument("--modes", default="single,batch,merged")
     ap.add_argument("--no-timing", action="store_true",
                     help="no KVD_OPT_TIMING events between launches (they break PDL adjacency)")
+    ap.add_argument("--early", type=int, default=1,
+                    help="KVD_OPT_EARLY_LOADS (1 default: the next pull's first ring of source "
+                         "reads overlaps the previous pull's tail)")
     ap.add_argument("--ipc", action="store_true",
                     help="prefill cache in a second process (CUDA IPC mapping, as deployed)")
     a = ap.parse_args()
@@ -92,6 +95,7 @@ def main():
         peer.set(kvd.OPT_STAGES, a.stages)
     if a.ctas:
         peer.set(kvd.OPT_MAX_CTAS, a.ctas)
+    peer.set(kvd.OPT_EARLY_LOADS, a.early)
     if not a.no_timing:
         peer.set(kvd.OPT_TIMING, 1)   # in-kernel %globaltimer spans of single pulls
     torch.cuda.set_device(a.dst_dev)
@@ -105,7 +109,7 @@ def main():
         nbytes = n * a.requests * g.num_layers * 2 * span
         res = {"config": a.config, "ipc": a.ipc, "tokens_per_request": t, "requests": a.requests,
                "bytes": nbytes, "opts": {"variant": a.variant, "threads": a.threads,
-                                         "stages": a.stages, "ctas": a.ctas}}
+                                         "stages": a.stages, "ctas": a.ctas, "early": a.early}}
         merged = (np.concatenate([s for s, _ in tables]), np.concatenate([d for _, d in tables]))
         for mode in a.modes.split(","):
             times = []
