@@ -52,6 +52,10 @@ import kvdgen  # noqa: E402
 METRIC = "KV pull GB/s per GPU pair vs 900 GB/s NVLink; p50 per-request transfer latency"
 NVLINK_NOMINAL_GBS = 900.0
 NVLINK_MEASURED_GBS = 770.0   # B200_PROFILING.md: measured peer copy per direction
+# NVLink 5 read user-data ceiling: 900 GB/s per direction on the wire, of which
+# every 128 B read response carries 16 B of protocol (ncu nvlrx__bytes_data_protocol
+# = 1/8 of nvlrx__bytes_data_user, profiles/ncu_pull_c2_nvlink.json) -> 900 * 128 / 144
+NVLINK_READ_USER_GBS = NVLINK_NOMINAL_GBS * 128.0 / 144.0
 C3_PAIRS = 4                  # C3 is defined on 4P:4D pairs; pair k gets requests i % 4 == k
 
 
@@ -703,13 +707,12 @@ def run_kvd(args, rank, world, local_rank):
     if multi:
         dist.all_gather_object(oks, bool(ok), group=gloo)
 
-    # Link-ceiling calibration (SURVEY §8 d; after the parity check, it
-    # overwrites destination blocks): a CONTIGUOUS request as large as the
-    # first request of a step, (i) read by the TMA bulk-copy ring on every SM
-    # (the SM/TMA contiguous peer-read ceiling) and (ii) copied by the copy
-    # engine over the same mapping (one cudaMemcpyAsync per (layer, K/V)
-    # segment, KVD_VARIANT_CE).  The better of the two is the measured
-    # denominator of the N >= 2 roofline.
+    # Link calibration (SURVEY §8 d; after the parity check, it overwrites
+    # destination blocks): a CONTIGUOUS request as large as the first
+    # request of a step, (i) read by the product's mover (auto policy: the
+    # TMA ring over NVLink) -- what the fragmented block table costs -- and
+    # (ii) copied by the copy engine over the same mapping (one
+    # cudaMemcpyAsync per (layer, K/V) segment, KVD_VARIANT_CE).
     ce_gbs = tma_gbs = None
     if peer and args.config != "c1":
         n0 = min(len(reqs[0][0]), g.num_blocks)
@@ -731,10 +734,8 @@ def run_kvd(args, rank, world, local_rank):
 
         peer.set(kvd.OPT_VARIANT, kvd.VARIANT_CE)
         ce_gbs = timed_contiguous()
-        if multi:
-            peer.set(kvd.OPT_VARIANT, kvd.VARIANT_TMA).set(kvd.OPT_MAX_CTAS, 1 << 16)
-            peer.set(kvd.OPT_THREADS, 32).set(kvd.OPT_STAGES, 6).set(kvd.OPT_TILE_BYTES, 32768)
-            tma_gbs = timed_contiguous()   # (the peer is only closed after this)
+        peer.set(kvd.OPT_VARIANT, {"lsu": 1, "lsu32": 2, "ce": 3, "tma": 4}.get(args.variant, 0))
+        tma_gbs = timed_contiguous()
 
     base = {}
     if multi and not args.no_nccl:
@@ -775,19 +776,13 @@ def run_kvd(args, rank, world, local_rank):
         achieved_link = float(np.mean(per_pair))
         bytes_per_step = dec[0]["bytes_per_step"]
         if multi:
-            # denominator: the ceiling measured in this run on contiguous data
-            # (TMA on every SM, or the copy engine, whichever is higher), else
-            # the guide's measured peer copy
-            calib = [max(s["tma_gbs"] or 0.0, s["ce_gbs"] or 0.0) for s in dec]
-            measured = float(np.mean(calib)) if all(calib) else None
-            peak = measured or NVLINK_MEASURED_GBS
+            peak = NVLINK_READ_USER_GBS
             roof = {"bound": "nvlink", "achieved": round(achieved_link, 1),
                     "peak": round(peak, 1), "unit": "GB/s",
                     "frac": round(achieved_link / peak, 4),
-                    "peak_source": ("measured in this run: contiguous request of the same size, "
-                                    "best of the TMA ring on every SM and the copy engine "
-                                    "(see calibration)") if measured else
-                                   "B200_PROFILING.md measured peer copy per direction",
+                    "peak_source": "NVLink 5 read user-data ceiling: 900 GB/s per direction x "
+                                   "128/144 (16 B protocol per 128 B read response, measured by "
+                                   "the ncu nvlrx counters in nvlink_rx)",
                     "frac_of_guide_770": round(achieved_link / NVLINK_MEASURED_GBS, 4),
                     "frac_of_nominal_900": round(achieved_link / NVLINK_NOMINAL_GBS, 4),
                     "algorithmic_bytes_per_step": bytes_per_step,
@@ -879,13 +874,13 @@ def run_kvd(args, rank, world, local_rank):
             "calibration": {
                 "copy_engine_gbs_per_pair": (round(float(np.mean([s["ce_gbs"] for s in dec])), 1)
                                              if all(s["ce_gbs"] for s in dec) else None),
-                "tma_contiguous_gbs_per_pair": (
+                "mover_contiguous_gbs_per_pair": (
                     round(float(np.mean([s["tma_gbs"] for s in dec])), 1)
                     if all(s["tma_gbs"] for s in dec) else None),
                 "what": "a contiguous request as large as the first request of a step over the "
                         "same mapping: (copy engine) one cudaMemcpyAsync per (layer, K/V) "
-                        "segment; (tma) the TMA bulk-copy ring on every SM, 6 x 32 KiB stages "
-                        "per CTA -- the link ceiling the paged pull is measured against"},
+                        "segment; (tma) the product's own mover and launch policy -- how much "
+                        "the fragmented block table costs"},
             "parity": bool(all(oks)),
             "clocks": clk,
         }
@@ -981,6 +976,8 @@ def main():
         import torch
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        # the NCCL baselines' send/recv are serialised by design (one pair)
+        os.environ.setdefault("TORCH_NCCL_SHOW_EAGER_INIT_P2P_SERIALIZATION_WARNING", "false")
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         if world % 2:

@@ -163,15 +163,15 @@ typedef enum {
                                kvd_wait_done (the paper's decode worker polls) or order a
                                stream after it with kvd_stream_wait.  Changing it synchronises the
                                library streams */
-  KVD_OPT_EARLY_LOADS = 9   /* 1 (default): a pull over NVLink with the TMA mover reads its first
-                               ring of SOURCE blocks before the preceding kernel on the stream
-                               has finished (programmatic dependent launch), so consecutive
-                               pulls overlap ramp and tail; its stores into the decode cache
-                               still wait for that kernel.  The caller guarantees that the
-                               source blocks are not written by work queued earlier on the same
-                               stream (in the paper's flow they are the prefill worker's
-                               finished cache, written by another process).  0: every
-                               access waits (strict stream order) */
+  KVD_OPT_EARLY_LOADS = 9   /* k in [0, 8], default 2: a pull with the TMA mover reads the first
+                               k stages of every pipe's ring from the SOURCE before the
+                               preceding kernel on the stream has finished (programmatic
+                               dependent launch), so consecutive pulls overlap ramp and tail;
+                               its stores into the decode cache still wait for that kernel.
+                               The caller guarantees that the source blocks are not written by
+                               work queued earlier on the same stream (in the paper's flow they
+                               are the prefill worker's finished cache, written by another
+                               process).  0: every access waits (strict stream order) */
 } kvd_option;
 
 typedef struct kvd_cache_s* kvd_cache;
@@ -411,6 +411,23 @@ KVD_API kvd_status kvd_peer_device_time(kvd_peer peer, double* total_ms, uint64_
  * are then already in the caller's stream order).  Errors: KVD_EINVAL,
  * KVD_ECUDA. */
 KVD_API kvd_status kvd_stream_wait(kvd_peer peer, void* stream);
+
+/* %globaltimer timeline of one retired single pull (KVD_OPT_TIMING), in the
+ * decode GPU's nanosecond timer: the earliest CTA start, the earliest return
+ * from the wait for the preceding kernel on the stream (after early source
+ * reads, KVD_OPT_EARLY_LOADS; else = start), and the last CTA's completion
+ * right before the slot word's release. */
+typedef struct {
+  uint64_t request_id;
+  uint64_t start_ns;
+  uint64_t wait_ns;
+  uint64_t end_ns;
+} kvd_span;
+
+/* Diagnostics: the timelines of the timed single pulls retired (by any
+ * poller) since the previous call, oldest first, at most `cap` (and at most
+ * the 4096 most recent); *n = how many were written. */
+KVD_API kvd_status kvd_peer_spans(kvd_peer peer, kvd_span* out, uint32_t cap, uint32_t* n);
 
 /* Describe the most recent kvd_pull on this peer. */
 KVD_API kvd_status kvd_last_pull_info(kvd_peer peer, kvd_pull_info* out);

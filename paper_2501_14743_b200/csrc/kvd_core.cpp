@@ -617,7 +617,11 @@ struct kvd_peer_s {
   uint32_t stages = 4;                      // TMA ring depth (auto TMA: 6)
   bool stages_set = false;
   int coalesce = 1;
-  bool early_loads = true;                  // KVD_OPT_EARLY_LOADS
+  // KVD_OPT_EARLY_LOADS: ring stages read before the wait.  The preceding
+  // grid's completion also waits for these reads to land, so a short early
+  // window (2 stages) beats the whole ring: 10 MB back-to-back pulls 417 ->
+  // 482 GB/s vs 455 with all 6 (profiles/r02_timeline_early_depth.jsonl)
+  uint32_t early_loads = 2;
   int variant = KVD_VARIANT_AUTO;
   int sm_count = 148;
 
@@ -631,9 +635,15 @@ struct kvd_peer_s {
   bool timing = false;                      // KVD_OPT_TIMING != 0: %globaltimer spans
   bool timing_events = false;               // KVD_OPT_TIMING == 1: also CUDA events per launch
   unsigned int* tile_ctrs = nullptr;        // per-slot dynamic tile counters (device, 0 idle)
-  unsigned long long* gt_start = nullptr;   // per-slot earliest CTA start (device, ~0 idle)
-  unsigned long long* gt_host = nullptr;    // per-slot duration ns (pinned, host-mapped)
+  unsigned long long* gt_start = nullptr;   // per slot {earliest start, earliest wait} (device, ~0 idle)
+  unsigned long long* gt_host = nullptr;    // per slot {duration, start, wait, end} ns (pinned, mapped)
   unsigned long long* gt_dev = nullptr;
+  // timeline of retired timed requests (kvd_peer_spans): a ring written by
+  // whichever poller retires a request, read by kvd_peer_spans
+  static constexpr uint32_t kSpanRing = 4096;
+  std::unique_ptr<kvd_span[]> spans;
+  std::atomic<uint64_t> span_count{0};
+  std::atomic<uint64_t> span_read{0};
   std::atomic<uint64_t> gt_ns{0};           // summed durations of retired timed requests
   std::atomic<uint64_t> gt_count{0};
   // KVD_OPT_STREAMS >= 2: transfers fork off the caller's stream onto these
@@ -1127,11 +1137,12 @@ static kvd_status open_impl(kvd_cache local, const void* blob, size_t blob_len,
   KVD_CUDA(cudaMemset(p->bytectr, 0, kSlots * sizeof(unsigned long long)));
   KVD_CUDA(cudaMalloc(&p->tile_ctrs, kSlots * sizeof(unsigned int)));
   KVD_CUDA(cudaMemset(p->tile_ctrs, 0, kSlots * sizeof(unsigned int)));
-  KVD_CUDA(cudaMalloc(&p->gt_start, kSlots * sizeof(unsigned long long)));
-  KVD_CUDA(cudaMemset(p->gt_start, 0xff, kSlots * sizeof(unsigned long long)));
-  KVD_CUDA(cudaHostAlloc((void**)&p->gt_host, kSlots * sizeof(unsigned long long),
+  KVD_CUDA(cudaMalloc(&p->gt_start, 2 * kSlots * sizeof(unsigned long long)));
+  KVD_CUDA(cudaMemset(p->gt_start, 0xff, 2 * kSlots * sizeof(unsigned long long)));
+  KVD_CUDA(cudaHostAlloc((void**)&p->gt_host, 4 * kSlots * sizeof(unsigned long long),
                          cudaHostAllocMapped | cudaHostAllocPortable));
-  memset(p->gt_host, 0, kSlots * sizeof(unsigned long long));
+  memset(p->gt_host, 0, 4 * kSlots * sizeof(unsigned long long));
+  p->spans.reset(new kvd_span[kvd_peer_s::kSpanRing]());
   KVD_CUDA(cudaHostGetDevicePointer((void**)&p->gt_dev, p->gt_host, 0));
   KVD_CUDA(cudaDeviceSynchronize());
   p->slots.reset(new kvd_peer_s::Slot[kSlots]);
@@ -1180,7 +1191,9 @@ kvd_status kvd_peer_set(kvd_peer p, int option, int64_t value) {
       p->coalesce = value ? 1 : 0;
       return KVD_OK;
     case KVD_OPT_EARLY_LOADS:
-      p->early_loads = value != 0;
+      if (value < 0 || value > (int64_t)kvd::max_stages())
+        return fail(KVD_EINVAL, "early loads must be in [0, %u] ring stages", kvd::max_stages());
+      p->early_loads = (uint32_t)value;
       return KVD_OK;
     case KVD_OPT_VARIANT:
       if (value < KVD_VARIANT_AUTO || value > KVD_VARIANT_TMA)
@@ -1499,8 +1512,15 @@ static bool slot_retire(kvd_peer_s* p, uint32_t i, uint64_t token) {
                                        std::memory_order_acquire))
     return false;
   if (S.timed) {   // written by the kernel before the slot word's release
-    p->gt_ns.fetch_add(__atomic_load_n(&p->gt_host[i], __ATOMIC_RELAXED), std::memory_order_relaxed);
+    const unsigned long long* g = p->gt_host + 4 * (size_t)i;
+    p->gt_ns.fetch_add(__atomic_load_n(&g[0], __ATOMIC_RELAXED), std::memory_order_relaxed);
     p->gt_count.fetch_add(1, std::memory_order_relaxed);
+    const uint64_t k = p->span_count.fetch_add(1, std::memory_order_relaxed);
+    kvd_span& sp = p->spans[k % kvd_peer_s::kSpanRing];
+    sp.request_id = S.rid.load(std::memory_order_relaxed);
+    sp.start_ns = g[1];
+    sp.wait_ns = g[2];
+    sp.end_ns = g[3];
   }
   S.state.store(0, std::memory_order_release);
   return true;
@@ -1578,8 +1598,8 @@ static kvd_status transfer(kvd_peer p, uint64_t request_id, const int32_t* src_i
   a.dst_layer_bytes = dg_.layer_bytes;
   const bool timed = p->timing && n > 0 && variant != KVD_VARIANT_CE;
   if (timed) {
-    a.gt_start = p->gt_start + slot;
-    a.gt_out = p->gt_dev + slot;
+    a.gt_start = p->gt_start + 2 * (size_t)slot;
+    a.gt_out = p->gt_dev + 4 * (size_t)slot;
   }
 
   DeviceGuard dgd(p->local->device);
@@ -1644,7 +1664,7 @@ static kvd_status transfer(kvd_peer p, uint64_t request_id, const int32_t* src_i
     if (variant == KVD_VARIANT_TMA && !p->row_bytes) {
       a.tile_ctr = p->tile_ctrs + slot;
       // the next pull's source reads overlap this one's tail
-      a.early_loads = (p->early_loads && !push && p->remote_device != p->local->device) ? 1u : 0u;
+      a.early_loads = push ? 0u : p->early_loads;
     }
     timing_begin(p, stream);
     e = kvd::launch_pull(a, p->runs4.data(), variant, ctas, threads, pol.stages, stream);
@@ -2027,6 +2047,18 @@ kvd_status kvd_peer_device_time(kvd_peer p, double* total_ms, uint64_t* launches
   if (!p || !total_ms || !launches) return fail(KVD_EINVAL, "null argument");
   *total_ms = (double)p->gt_ns.exchange(0, std::memory_order_relaxed) * 1e-6;
   *launches = p->gt_count.exchange(0, std::memory_order_relaxed);
+  return KVD_OK;
+}
+
+kvd_status kvd_peer_spans(kvd_peer p, kvd_span* out, uint32_t cap, uint32_t* n) {
+  if (!p || !n || (cap && !out)) return fail(KVD_EINVAL, "null argument");
+  const uint64_t end = p->span_count.load(std::memory_order_acquire);
+  uint64_t k = p->span_read.load(std::memory_order_relaxed);
+  if (end - k > kvd_peer_s::kSpanRing) k = end - kvd_peer_s::kSpanRing;   // oldest overwritten
+  uint32_t m = 0;
+  for (; k < end && m < cap; ++k) out[m++] = p->spans[k % kvd_peer_s::kSpanRing];
+  p->span_read.store(k, std::memory_order_relaxed);
+  *n = m;
   return KVD_OK;
 }
 

@@ -72,10 +72,12 @@ struct PullArgs {
   // lie inside their layer tensors, counts violations here and skips them.
   unsigned int* audit;
   unsigned long long src_layer_bytes, dst_layer_bytes;
-  // Device-side duration (KVD_OPT_TIMING, single pulls): every CTA
-  // atomicMin's its %globaltimer start into *gt_start (reset to ~0 by the
-  // last CTA); the last CTA writes end - start (ns) to *gt_out (pinned,
-  // host-mapped) before it releases the slot word.  nullptr: off.
+  // Device-side timeline (KVD_OPT_TIMING, single pulls), %globaltimer ns:
+  // every CTA atomicMin's its start into gt_start[0]; the pipes that read
+  // early atomicMin the moment their griddepcontrol.wait returned into
+  // gt_start[1] (the others: their start); the last CTA writes {end - start,
+  // start, wait, end} to gt_out[0..3] (pinned, host-mapped) before it
+  // releases the slot word and resets gt_start to ~0.  nullptr: off.
   unsigned long long* gt_start;
   unsigned long long* gt_out;
   // TMA single pulls: per-slot tile counter (device, zero at launch) from
@@ -83,10 +85,11 @@ struct PullArgs {
   // static grid-stride order.
   unsigned int* tile_ctr;
   // TMA single pulls over NVLink: lane 0 of each pipe claims and issues its
-  // first ring of bulk loads from the SOURCE before griddepcontrol.wait, so
-  // the ramp of a pull overlaps the drain and completion tail of the pull
-  // before it on the stream.  Only the source (the prefill's finished cache)
-  // is read early; every store into the decode cache waits.
+  // first early_loads ring stages of bulk loads from the SOURCE before
+  // griddepcontrol.wait (0: none), so the ramp of a pull overlaps the drain
+  // and completion tail of the pull before it on the stream.  Only the
+  // source (the prefill's finished cache) is read early; every store into
+  // the decode cache waits.
   unsigned int early_loads;
   // Batches: the launch's own arrival/tile counters live with its
   // descriptor buffer; the last CTA resets them and then releases done_seq

@@ -122,9 +122,17 @@ __device__ __forceinline__ void pdl_trigger() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-// KVD_OPT_TIMING: the earliest CTA start of this launch (see PullArgs::gt_start)
-__device__ __forceinline__ void mark_start(const PullArgs& a) {
-  if (a.gt_start != nullptr && threadIdx.x == 0) atomicMin(a.gt_start, globaltimer());
+// KVD_OPT_TIMING: the earliest CTA start of this launch, and the earliest
+// return from griddepcontrol.wait (see PullArgs::gt_start)
+__device__ __forceinline__ void mark_start(const PullArgs& a, bool waited) {
+  if (a.gt_start != nullptr && threadIdx.x == 0) {
+    const unsigned long long t = globaltimer();
+    atomicMin(a.gt_start, t);
+    if (waited) atomicMin(a.gt_start + 1, t);
+  }
+}
+__device__ __forceinline__ void mark_wait(const PullArgs& a) {
+  if (a.gt_start != nullptr) atomicMin(a.gt_start + 1, globaltimer());
 }
 
 // One warp copies `bytes` (multiple of sizeof(V)) from src to dst.  All U
@@ -419,8 +427,15 @@ __device__ __forceinline__ void complete(const PullArgs& a) {
       }
       if (a.gt_start != nullptr) {   // first CTA start -> last CTA done, before the release
         const unsigned long long t1 = globaltimer();
-        *(volatile unsigned long long*)a.gt_out = t1 - *(volatile unsigned long long*)a.gt_start;
-        *a.gt_start = ~0ull;
+        const unsigned long long t0 = *(volatile unsigned long long*)a.gt_start;
+        const unsigned long long tw = *(volatile unsigned long long*)(a.gt_start + 1);
+        volatile unsigned long long* o = a.gt_out;
+        o[0] = t1 - t0;
+        o[1] = t0;
+        o[2] = tw;
+        o[3] = t1;
+        a.gt_start[0] = ~0ull;
+        a.gt_start[1] = ~0ull;
       }
       publish_token(a, a.flag, a.token, a.request_id, a.mbox_pos);
     }
@@ -454,7 +469,7 @@ pull_kernel(const __grid_constant__ PullParams<MAXR> P) {
   extern __shared__ int4 s_runs[];
   const PullArgs& a = P.a;
   pdl_wait();
-  mark_start(a);
+  mark_start(a, true);
   const int4* runs = stage_runs(a, (MAXR > 0) ? P.runs : a.runs_dev, s_runs);
   const unsigned int lane = threadIdx.x & 31u;
   const unsigned int warps_per_cta = blockDim.x >> 5;
@@ -553,7 +568,7 @@ pull_kernel_tma(const __grid_constant__ PullParams<MAXR> P, unsigned int stages)
   // open), this launch's tile counter and the SOURCE blocks.
   const bool early = a.early_loads != 0;
   if (!early) pdl_wait();
-  mark_start(a);
+  mark_start(a, !early);
   const unsigned int warp = threadIdx.x >> 5;
   const unsigned int pipes_per_cta = blockDim.x >> 5;
   const unsigned int npipes = gridDim.x * pipes_per_cta;
@@ -588,16 +603,29 @@ pull_kernel_tma(const __grid_constant__ PullParams<MAXR> P, unsigned int stages)
     // instead: a pipe claims kClaim consecutive tiles at a time,
     // so the pipes finish within a few tiles of each other (no static
     // imbalance at the tail) and the front still sweeps the request in order.
+    // The first ring needs no atomic: tiles [0, npipes * S) are dealt
+    // statically, S consecutive ones per pipe, and the counter hands out the
+    // rest.  Each pipe keeps one claim in flight ahead of need (issued when
+    // it starts on the previous block), so a claim's round trip to L2 never
+    // stalls the ring.
     constexpr unsigned int kNone = 0xffffffffu;
-    const unsigned int kClaim = a.nreqs ? K : 4u;   // batches: claim credit-friendly groups
-    unsigned int handed = 0, cur = 0, cur_end = 0;
+    const unsigned int kClaim = a.nreqs ? K : 2u;   // batches: claim credit-friendly groups
+    const unsigned int dealt = min(npipes * S, a.total_tiles);
+    unsigned int handed = 0, cur = min(pipe * S, dealt), cur_end = min(pipe * S + S, dealt);
+    unsigned int ahead = 0;
+    bool have_ahead = false;
     auto next = [&]() -> unsigned int {
       if (a.tile_ctr == nullptr) return handed < count ? tile_of(handed++) : kNone;
       if (cur == cur_end) {
-        const unsigned int base = atomicAdd(a.tile_ctr, kClaim);
+        const unsigned int base = have_ahead ? ahead : dealt + atomicAdd(a.tile_ctr, kClaim);
+        ahead = dealt + atomicAdd(a.tile_ctr, kClaim);   // consumed a block from now
+        have_ahead = true;
         if (base >= a.total_tiles) return kNone;
         cur = base;
         cur_end = min(base + kClaim, a.total_tiles);
+      } else if (!have_ahead && cur + 1 == cur_end) {
+        ahead = dealt + atomicAdd(a.tile_ctr, kClaim);     // ahead of the first dynamic block
+        have_ahead = true;
       }
       return cur++;
     };
@@ -627,7 +655,20 @@ pull_kernel_tma(const __grid_constant__ PullParams<MAXR> P, unsigned int stages)
       }
       return t;
     };
+    // the first a.early_loads stages are loaded before the wait (the
+    // preceding grid's completion also waits for these reads to land, so
+    // the early window is sized to its tail, not to the whole ring)
+    auto wait_preceding = [&]() {            // stores below: the preceding grid is done
+      pdl_wait();
+      mark_wait(a);
+      waited = true;
+      if (exhausted && !triggered) {
+        pdl_trigger();
+        triggered = true;
+      }
+    };
     for (unsigned int k = 0; k < S; ++k) {
+      if (!waited && k == a.early_loads) wait_preceding();
       const unsigned int t = claim();
       if (t == kNone) break;
       tiles[k] = audited(a, tile_at(a, runs, t), t);
@@ -635,14 +676,7 @@ pull_kernel_tma(const __grid_constant__ PullParams<MAXR> P, unsigned int stages)
                &bar[k]);
       ++issued;
     }
-    if (early) {                             // stores below: the preceding grid is done
-      pdl_wait();
-      waited = true;
-      if (exhausted && !triggered) {
-        pdl_trigger();
-        triggered = true;
-      }
-    }
+    if (!waited) wait_preceding();
     for (unsigned int i = 0; i < issued; ++i) {
       const unsigned int s = i % S;
       mbar_wait(&bar[s], (i / S) & 1u);
@@ -693,7 +727,7 @@ pull_kernel_tma_rows(const __grid_constant__ PullParams<MAXR> P, unsigned int st
   __shared__ uint64_t bars[(256 / 32) * kMaxStages];
   const PullArgs& a = P.a;
   pdl_wait();
-  mark_start(a);
+  mark_start(a, true);
   const unsigned int lane = threadIdx.x & 31u;
   const unsigned int warp = threadIdx.x >> 5;
   const unsigned int pipes_per_cta = blockDim.x >> 5;

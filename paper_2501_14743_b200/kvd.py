@@ -32,6 +32,7 @@ EXPORTED = (
     "kvd_peer_set", "kvd_pull", "kvd_push", "kvd_pull_batch", "kvd_poll_done", "kvd_wait_done",
     "kvd_poll_many",
     "kvd_last_pull_info", "kvd_peer_audit", "kvd_peer_kernel_time", "kvd_peer_device_time",
+    "kvd_peer_spans",
     "kvd_stream_wait",
     "kvd_poll_released",
     "kvd_gather", "kvd_scatter", "kvd_strerror", "kvd_last_error", "kvd_abi_version",
@@ -65,6 +66,11 @@ class kvd_pull_info(ctypes.Structure):
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class kvd_span(ctypes.Structure):
+    _fields_ = [("request_id", ctypes.c_uint64), ("start_ns", ctypes.c_uint64),
+                ("wait_ns", ctypes.c_uint64), ("end_ns", ctypes.c_uint64)]
 
 
 class KvdError(RuntimeError):
@@ -122,6 +128,7 @@ _SIGS = {
     "kvd_poll_released": [_p, _p, _u32, ctypes.POINTER(_u32)],
     "kvd_peer_kernel_time": [_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_u64)],
     "kvd_peer_device_time": [_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_u64)],
+    "kvd_peer_spans": [_p, _p, _u32, ctypes.POINTER(_u32)],
     "kvd_stream_wait": [_p, _p],
     "kvd_gather": [_p, _pi32, _u32, _p, _p],
     "kvd_scatter": [_p, _pi32, _u32, _p, _p],
@@ -369,6 +376,16 @@ def kvd_peer_device_time(peer: int):
     _check(_lib.kvd_peer_device_time(peer, ctypes.byref(ms), ctypes.byref(n)),
            "kvd_peer_device_time")
     return ms.value, n.value
+
+
+def kvd_peer_spans(peer: int, cap: int = 4096) -> list:
+    """[(request_id, start_ns, wait_ns, end_ns)] of the timed single pulls
+    retired since the previous call (%globaltimer of the decode GPU)."""
+    buf = (kvd_span * max(1, cap))()
+    n = _u32(0)
+    _check(_lib.kvd_peer_spans(peer, ctypes.cast(buf, _p), cap, ctypes.byref(n)), "kvd_peer_spans")
+    return [(buf[i].request_id, buf[i].start_ns, buf[i].wait_ns, buf[i].end_ns)
+            for i in range(n.value)]
 
 
 def kvd_stream_wait(peer: int, stream: int) -> None:

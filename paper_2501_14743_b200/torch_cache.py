@@ -155,6 +155,11 @@ class Peer:
         retired single pulls since the last call; needs OPT_TIMING."""
         return kvd.kvd_peer_device_time(self.handle)
 
+    def spans(self) -> list:
+        """[(request_id, start_ns, wait_ns, end_ns)] %globaltimer timelines of the
+        timed single pulls retired since the last call; needs OPT_TIMING."""
+        return kvd.kvd_peer_spans(self.handle)
+
     def stream_wait(self, stream: Optional[torch.cuda.Stream] = None) -> None:
         """With OPT_STREAMS >= 2: order `stream` after every transfer issued so far."""
         s = stream if stream is not None else torch.cuda.current_stream(self.local.device)

@@ -486,3 +486,72 @@ def test_back_to_back_pulls_keep_stream_order(variant):
             assert_layers_equal(pair.download_dst(), pair.expected(s2, d, zero))
     finally:
         pair.close()
+
+
+@pytest.mark.parametrize("early", [0, 2, 8])
+def test_early_source_reads_keep_destination_order(early):
+    """KVD_OPT_EARLY_LOADS: a TMA pull may read its SOURCE before the kernel
+    ahead of it on the stream has finished, but every store into the
+    destination still follows that kernel: a pull right behind another pull
+    into the same blocks (write after write), behind a kernel zeroing the
+    destination, lands last -- for every early-read depth."""
+    g = kvdgen.CacheGeom(4, 8, 128, 16, 512, kvdgen.FP16)      # 32 KiB spans
+    pair = make_pair(g, g, seed=42)
+    try:
+        pair.peer.set(kvd.OPT_VARIANT, kvd.VARIANT_TMA).set(kvd.OPT_EARLY_LOADS, early)
+        rng = np.random.default_rng(4)
+        d = rng.choice(512, size=300, replace=False).astype(np.int32)
+        st = torch.cuda.Stream()
+        for _ in range(5):
+            s1 = rng.choice(512, size=300, replace=False).astype(np.int32)
+            s2 = rng.choice(512, size=300, replace=False).astype(np.int32)
+            with torch.cuda.stream(st):
+                for t in pair.dst.layers:
+                    t.zero_()
+            r1, r2 = next_request_id(), next_request_id()
+            pair.peer.pull(r1, s1, d, st)
+            pair.peer.pull(r2, s2, d, st)
+            pair.peer.wait(r1)
+            pair.peer.wait(r2)
+            st.synchronize()
+            zero = [np.zeros_like(h) for h in pair.dst_host]
+            assert_layers_equal(pair.download_dst(), pair.expected(s2, d, zero))
+    finally:
+        pair.close()
+
+
+def test_strict_order_chains_pulls():
+    """KVD_OPT_EARLY_LOADS = 0 is strict stream order for the source too: a
+    pull whose SOURCE is the destination of the pull right before it on the
+    same stream (A -> B, then B -> C) reads the bytes the first one wrote."""
+    g = kvdgen.CacheGeom(4, 8, 128, 16, 256, kvdgen.FP16)
+    ab = make_pair(g, g, seed=43)
+    from gpu_helpers import cache_for
+    c = cache_for(g, 0)
+    try:
+        bc = c.open_peer(ab.dst.export())
+        for p in (ab.peer, bc):
+            p.set(kvd.OPT_VARIANT, kvd.VARIANT_TMA).set(kvd.OPT_EARLY_LOADS, 0)
+        s, d = kvdgen.fragmented_table(200, 256, 256, seed=8)
+        s2, d2 = kvdgen.fragmented_table(200, 256, 256, seed=9)
+        st = torch.cuda.Stream()
+        for t in c.layers:
+            t.zero_()
+        torch.cuda.synchronize()
+        r1, r2 = next_request_id(), next_request_id()
+        ab.peer.pull(r1, s, d, st)
+        bc.pull(r2, d[:150], d2[:150], st)     # reads blocks the first pull writes
+        ab.peer.wait(r1)
+        bc.wait(r2)
+        st.synchronize()
+        mid = ab.expected(s, d)
+        from oracle import oracle
+        want = [np.zeros(c.layer_bytes, np.uint8) for _ in range(g.num_layers)]
+        rc = oracle.pull(mid, g.stride, g.num_blocks, want, g.stride, g.num_blocks,
+                         g.num_kv_heads, g.head_dim, g.block_size, g.elem_bytes, d[:150], d2[:150])
+        assert rc == oracle.OK
+        assert_layers_equal([t.cpu().numpy() for t in c.layers], want)
+        bc.close()
+    finally:
+        c.close()
+        ab.close()

@@ -4,7 +4,8 @@
 //
 //   nvcc -O2 -I include tools/native/kvd_latency.cu -L paper_2501_14743_b200 -lkvd \
 //        -Xlinker -rpath=$PWD/paper_2501_14743_b200 -o tools/native/kvd_latency
-//   tools/native/kvd_latency [src_dev] [dst_dev] [iters]
+//   tools/native/kvd_latency [src_dev] [dst_dev] [iters] [timing 0|1]
+// timing 1 also reports the in-kernel %globaltimer span (KVD_OPT_TIMING = 2).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -45,7 +46,8 @@ static Cache make(int dev, const kvd_layout& L) {
   return c;
 }
 
-static void run(const char* name, const kvd_layout& L, uint32_t n, int sdev, int ddev, int iters) {
+static void run(const char* name, const kvd_layout& L, uint32_t n, int sdev, int ddev, int iters,
+                bool timing) {
   Cache src = make(sdev, L), dst = make(ddev, L);
   std::vector<unsigned char> blob(1 << 16);
   size_t len = blob.size();
@@ -60,7 +62,8 @@ static void run(const char* name, const kvd_layout& L, uint32_t n, int sdev, int
     si[i] = (int32_t)(2 * i % L.num_blocks);
     di[i] = (int32_t)((2 * i + 1) % L.num_blocks);
   }
-  std::vector<double> lat, call;
+  std::vector<double> lat, call, span;
+  if (timing) CK(kvd_peer_set(p, KVD_OPT_TIMING, 2));   // in-kernel %globaltimer spans
   for (int it = 0; it < iters + 20; ++it) {
     const uint64_t rid = 100 + it;
     auto t0 = std::chrono::steady_clock::now();
@@ -73,7 +76,14 @@ static void run(const char* name, const kvd_layout& L, uint32_t n, int sdev, int
       call.push_back(std::chrono::duration<double, std::micro>(t1 - t0).count());
       lat.push_back(std::chrono::duration<double, std::micro>(t2 - t0).count());
     }
+    if (timing) {
+      kvd_span sp;
+      uint32_t k = 0;
+      CK(kvd_peer_spans(p, &sp, 1, &k));
+      if (k && it >= 20) span.push_back((sp.end_ns - sp.start_ns) * 1e-3);
+    }
   }
+  std::sort(span.begin(), span.end());
   std::sort(lat.begin(), lat.end());
   std::sort(call.begin(), call.end());
   auto q = [](const std::vector<double>& v, double f) { return v[(size_t)(f * (v.size() - 1))]; };
@@ -81,9 +91,9 @@ static void run(const char* name, const kvd_layout& L, uint32_t n, int sdev, int
   kvd_last_pull_info(p, &info);
   printf("{\"config\": \"%s\", \"src_dev\": %d, \"dst_dev\": %d, \"bytes\": %llu, \"variant\": %u, "
          "\"ctas\": %u, \"call_us_p50\": %.2f, \"latency_us_p50\": %.2f, \"latency_us_p90\": %.2f, "
-         "\"latency_us_min\": %.2f, \"iters\": %d}\n",
+         "\"latency_us_min\": %.2f, \"kernel_span_us_p50\": %.2f, \"iters\": %d}\n",
          name, sdev, ddev, (unsigned long long)info.bytes, info.variant, info.ctas, q(call, 0.5),
-         q(lat, 0.5), q(lat, 0.9), lat.front(), iters);
+         q(lat, 0.5), q(lat, 0.9), lat.front(), span.empty() ? -1.0 : q(span, 0.5), iters);
   kvd_close_peer(p);
   kvd_unregister_cache(dst.h);
   kvd_unregister_cache(src.h);
@@ -95,9 +105,10 @@ int main(int argc, char** argv) {
   const int sdev = argc > 1 ? atoi(argv[1]) : 0;
   const int ddev = argc > 2 ? atoi(argv[2]) : 0;
   const int iters = argc > 3 ? atoi(argv[3]) : 2000;
+  const bool timing = argc > 4 && atoi(argv[4]) != 0;
   kvd_layout c1{2, 2, 64, 16, 64, KVD_FP16, {0, 0, 0, 0, 0}};
-  run("C1", c1, 16, sdev, ddev, iters);
+  run("C1", c1, 16, sdev, ddev, iters, timing);
   kvd_layout c2{32, 32, 128, 16, 1024, KVD_FP16, {0, 0, 0, 0, 0}};
-  run("C2", c2, 512, sdev, ddev, std::max(20, iters / 50));
+  run("C2", c2, 512, sdev, ddev, std::max(20, iters / 50), timing);
   return 0;
 }
