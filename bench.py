@@ -684,6 +684,24 @@ def run_kvd(args, rank, world, local_rank):
     if peer and n_req > 1:
         for _ in range(3):
             step(lat_queued)
+    # --engine C: the same isolated requests posted to the resident pull
+    # engine (KVD_OPT_ENGINE; no launch per request, not stream-ordered)
+    lat_engine = []
+    if args.engine:
+        if peer:
+            peer.set(kvd.OPT_ENGINE, args.engine)
+        for _ in range(reps):
+            for s_, d_ in reqs:
+                if multi:
+                    dist.barrier(group=gloo)
+                if peer:
+                    rid[0] += 1
+                    t0 = time.perf_counter_ns()
+                    peer.pull(rid[0], s_, d_, stream)
+                    peer.wait(rid[0])
+                    lat_engine.append(time.perf_counter_ns() - t0)
+        if peer:
+            peer.set(kvd.OPT_ENGINE, 0)
 
     info = peer.info() if peer else {}
     dev_s = t_start.elapsed_time(t_end) / 1e3 if peer else 0.0
@@ -753,7 +771,7 @@ def run_kvd(args, rank, world, local_rank):
              "gt_ms_total": gt_ms_total, "gt_launches": gt_launches,
              "lat": lat_ns, "clock": sampler.summary(), "info": info, "base": base,
              "launches": timed_launches, "runs": info.get("runs"), "ce_gbs": ce_gbs,
-             "tma_gbs": tma_gbs, "lat_queued": lat_queued,
+             "tma_gbs": tma_gbs, "lat_queued": lat_queued, "lat_engine": lat_engine,
              "bytes_per_step": bytes_per_step if peer else 0}
     all_stats = cluster.gather_stats(stats, gloo) if multi else [stats]
 
@@ -766,6 +784,9 @@ def run_kvd(args, rank, world, local_rank):
         # once; its latency is the slowest shard's (SURVEY §8 d)
         lat_req = ([max(col) for col in zip(*[s["lat"] for s in dec])]
                    if args.config == "c4" and len(dec) > 1 else lat_all)
+        engine_req = ([max(col) for col in zip(*[s["lat_engine"] for s in dec])]
+                      if args.config == "c4" and len(dec) > 1
+                      else [x for s in dec for x in s["lat_engine"]])
         step_dev = max(s["step_ms"] for s in dec)
         info0 = dec[0]["info"]
         peaks, peak_src = measured_peaks()
@@ -862,7 +883,15 @@ def run_kvd(args, rank, world, local_rank):
                                   if dec[0]["lat_queued"] else None),
                 "queued_what": ("the pair's requests issued together as in a timed step, "
                                 "issue -> completion observed (includes queueing)")
-                               if dec[0]["lat_queued"] else None},
+                               if dec[0]["lat_queued"] else None,
+                "engine_p50_ms": (round(nearest_rank(engine_req, 50) / 1e6, 4)
+                                  if engine_req else None),
+                "engine_p90_ms": (round(nearest_rank(engine_req, 90) / 1e6, 4)
+                                  if engine_req else None),
+                "engine_what": (f"--engine {args.engine}: the same isolated requests posted to "
+                                "the resident pull engine (KVD_OPT_ENGINE: no launch per "
+                                "request; requests > 2 MiB still launch)")
+                               if engine_req else None},
             "step_device_ms": round(step_dev, 4),
             "kernel_ms_per_step": round(kern_dev, 4),
             "roofline": roof,
@@ -959,6 +988,9 @@ def main():
     ap.add_argument("--memory", choices=["torch", "vmm"], default="torch",
                     help="cache memory: torch/cudaMalloc (legacy IPC) or kvd_mem_alloc (VMM, "
                          "POSIX-fd/fabric handles, §8 f3 groundwork)")
+    ap.add_argument("--engine", type=int, default=0,
+                    help="also time the isolated-request latency through the resident pull "
+                         "engine with this many CTAs (KVD_OPT_ENGINE)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-nccl", action="store_true", help="skip the NCCL send/recv baselines")
     args = ap.parse_args()

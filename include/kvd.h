@@ -163,7 +163,7 @@ typedef enum {
                                kvd_wait_done (the paper's decode worker polls) or order a
                                stream after it with kvd_stream_wait.  Changing it synchronises the
                                library streams */
-  KVD_OPT_EARLY_LOADS = 9   /* k in [0, 8], default 2: a pull with the TMA mover reads the first
+  KVD_OPT_EARLY_LOADS = 9,  /* k in [0, 8], default 2: a pull with the TMA mover reads the first
                                k stages of every pipe's ring from the SOURCE before the
                                preceding kernel on the stream has finished (programmatic
                                dependent launch), so consecutive pulls overlap ramp and tail;
@@ -172,6 +172,21 @@ typedef enum {
                                work queued earlier on the same stream (in the paper's flow they
                                are the prefill worker's finished cache, written by another
                                process).  0: every access waits (strict stream order) */
+  KVD_OPT_ENGINE = 10       /* c in [0, 8], default 0 (off): the resident pull engine for short
+                               requests -- one thread-block cluster of c CTAs (a persistent
+                               kernel) drains a ring of request descriptors the host writes
+                               into pinned memory (the paper's
+                               transaction queue, posted straight to the device), so
+                               a kvd_pull of <= 2 MiB in <= 64 runs (AUTO variant, not head-
+                               sliced) makes no CUDA call and pays no launch latency.  The
+                               engine is launched on the first such request and exits after
+                               2 ms without one (a watchdog thread), so it holds c SMs only
+                               while short requests flow.  Such requests are NOT ordered with
+                               the caller's stream (like KVD_OPT_STREAMS): the destination
+                               blocks must be free when kvd_pull is called, and completion is
+                               observed with kvd_poll_done / kvd_wait_done.  While the engine
+                               runs, a device-wide synchronise (cudaDeviceSynchronize) waits up
+                               to the idle timeout; synchronise streams instead.  0 stops it */
 } kvd_option;
 
 typedef struct kvd_cache_s* kvd_cache;

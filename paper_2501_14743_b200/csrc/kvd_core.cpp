@@ -26,6 +26,7 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <condition_variable>
 #include <mutex>
 #include <random>
 #include <thread>
@@ -653,6 +654,22 @@ struct kvd_peer_s {
   cudaEvent_t fork_event = nullptr;
   uint32_t next_stream = 0;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed, event_pool;
+  // resident pull engine (KVD_OPT_ENGINE): short requests
+  // are posted as descriptors into a pinned ring that a persistent kernel
+  // drains; it is launched on demand and told to exit after kEngineIdle of
+  // no posts (a watchdog thread), so it holds SMs only while requests flow
+  uint32_t engine_ctas = 0;                 // 0: off
+  bool engine_live = false;                 // a launch is draining the ring
+  int engine_variant = 0;
+  cudaStream_t engine_stream = nullptr;
+  unsigned long long* engine_ring = nullptr;  // pinned, mapped [kEngineRing][kEngineLLWords]
+  unsigned long long* engine_done = nullptr;
+  kvd::EngineParams engine_params{};
+  uint64_t engine_tail = 0;                 // next ring position
+  std::chrono::steady_clock::time_point engine_last;
+  std::thread engine_watch;
+  std::condition_variable engine_cv;
+  bool engine_quit = false;
   // §8 f4 head-sliced peer (row_bytes > 0): remote unit = block_size rows
   uint32_t row_bytes = 0;
   uint32_t dst_row_stride = 0;
@@ -961,8 +978,11 @@ kvd_status kvd_export_handle(kvd_cache c, void* blob, size_t* blob_len) {
   return KVD_OK;
 }
 
+static void engine_shutdown(kvd_peer p);
+
 static void peer_release(kvd_peer p) {
   if (!p) return;
+  engine_shutdown(p);   // a live engine would never let the device synchronise
   DeviceGuard dg(p->local ? p->local->device : 0);
   // pulls / pushes still in flight read or write through the mappings: let
   // them finish before anything is unmapped or freed (close is not hot)
@@ -1173,8 +1193,16 @@ kvd_status kvd_close_peer(kvd_peer p) {
   return KVD_OK;
 }
 
+static kvd_status engine_configure(kvd_peer p, uint32_t ctas);
+static void engine_quiesce(kvd_peer_s* p);
+
 kvd_status kvd_peer_set(kvd_peer p, int option, int64_t value) {
   if (!p) return fail(KVD_EINVAL, "null peer");
+  if (option == KVD_OPT_ENGINE) {   // takes the peer mutex itself (joins the watchdog)
+    if (value < 0 || value > (int64_t)kvd::kEngineMaxCtas)
+      return fail(KVD_EINVAL, "engine CTAs must be in [0, %u] (one cluster)", kvd::kEngineMaxCtas);
+    return engine_configure(p, (uint32_t)value);
+  }
   std::lock_guard<std::mutex> lk(p->mu);
   switch (option) {
     case KVD_OPT_MAX_CTAS:
@@ -1247,6 +1275,7 @@ kvd_status kvd_peer_set(kvd_peer p, int option, int64_t value) {
     case KVD_OPT_AUDIT: {
       DeviceGuard dg(p->local->device);
       if (!dg.ok) return fail(KVD_ECUDA, "cannot select device %d", p->local->device);
+      engine_quiesce(p);
       if (value && !p->audit_ctr) {
         KVD_CUDA(cudaMalloc(&p->audit_ctr, sizeof(unsigned int)));
         KVD_CUDA(cudaMemset(p->audit_ctr, 0, sizeof(unsigned int)));
@@ -1526,6 +1555,179 @@ static bool slot_retire(kvd_peer_s* p, uint32_t i, uint64_t token) {
   return true;
 }
 
+// The request-independent PullArgs fields of this peer's pull direction
+// (sides, unit, planes, tiling for `tile`).
+static kvd_status pair_args(const kvd_peer_s* p, uint32_t tile, kvd::PullArgs& a) {
+  const kvd_geometry& sg = p->remote.g;
+  const kvd_geometry& dg = p->local->geom.g;
+  a.src = kvd::SideAddr{p->d_src_bases, 0, 0, sg.plane_stride_bytes, sg.block_stride_bytes};
+  a.dst = kvd::SideAddr{p->local->d_bases, 0, 0, dg.plane_stride_bytes, dg.block_stride_bytes};
+  a.src_layer_bytes = sg.layer_bytes;
+  a.dst_layer_bytes = dg.layer_bytes;
+  std::vector<int4> r4;
+  return tile_runs(std::vector<kvd_run>{}, pair_plan(sg, dg), p->local->geom.layout.num_layers,
+                   tile, r4, a);
+}
+
+// ---------------------------------------------------------------------------
+// resident pull engine (KVD_OPT_ENGINE); peer mutex held unless noted
+// ---------------------------------------------------------------------------
+constexpr uint64_t kEngineMaxBytes = 2ull << 20;                  // launch path above this
+constexpr auto kEngineIdle = std::chrono::microseconds(2000);     // then the launch exits
+
+// Free ring position (its previous descriptor completed), else false.
+static bool engine_pos_free(const kvd_peer_s* p) {
+  const uint64_t pos = p->engine_tail;
+  return pos < kvd::kEngineRing ||
+         __atomic_load_n(&p->engine_done[pos % kvd::kEngineRing], __ATOMIC_ACQUIRE) ==
+             pos - kvd::kEngineRing + 1;
+}
+
+// Write the ring entry at the tail in the LL encoding (kvd_internal.h): every
+// 32-bit field as one atomic 64-bit word tagged with low32(position + 1);
+// the runs first, the header last.
+static void engine_publish(kvd_peer_s* p, const uint32_t* header, const int4* runs,
+                           uint32_t nruns) {
+  const uint64_t pos = p->engine_tail;
+  unsigned long long* w = p->engine_ring + (size_t)(pos % kvd::kEngineRing) * kvd::kEngineLLWords;
+  const uint64_t tag = (uint64_t)(uint32_t)(pos + 1) << 32;
+  const uint32_t* rv = reinterpret_cast<const uint32_t*>(runs);
+  for (uint32_t q = 0; q < 4 * nruns; ++q)
+    __atomic_store_n(&w[kvd::kEngineLLHeader + q], tag | rv[q], __ATOMIC_RELAXED);
+  for (uint32_t q = 0; q < kvd::kEngineLLHeader; ++q)
+    __atomic_store_n(&w[q], tag | header[q], __ATOMIC_RELEASE);
+  ++p->engine_tail;
+  p->engine_last = std::chrono::steady_clock::now();
+}
+
+// The running launch exits at the next ring position (requests already
+// posted complete first).
+static void engine_post_stop(kvd_peer_s* p) {
+  const uint64_t pos = p->engine_tail;
+  uint32_t header[kvd::kEngineLLHeader] = {};
+  header[7] = kvd::kEngineStop;
+  // nothing reads this position again before the next launch starts
+  __atomic_store_n(&p->engine_done[pos % kvd::kEngineRing], pos + 1, __ATOMIC_RELEASE);
+  engine_publish(p, header, nullptr, 0);
+  p->engine_live = false;
+}
+
+static cudaError_t engine_ensure_live(kvd_peer_s* p) {
+  if (p->engine_live) return cudaSuccess;
+  p->engine_params.first = p->engine_tail;
+  cudaError_t e = kvd::launch_engine(p->engine_params, p->engine_variant, p->engine_ctas,
+                                     p->engine_stream);
+  if (e == cudaSuccess) p->engine_live = true;
+  return e;
+}
+
+// Before a device-wide synchronise under the peer mutex: the running launch
+// exits at the next ring position (the watchdog cannot take the mutex).
+static void engine_quiesce(kvd_peer_s* p) {
+  if (p->engine_live) engine_post_stop(p);
+}
+
+// Lock NOT held: stop the watchdog and the running launch, free the ring.
+static void engine_shutdown(kvd_peer p) {
+  std::thread watch;
+  {
+    std::lock_guard<std::mutex> lk(p->mu);
+    if (!p->engine_ring) return;
+    p->engine_quit = true;
+    if (p->engine_live) engine_post_stop(p);
+    watch = std::move(p->engine_watch);
+  }
+  p->engine_cv.notify_all();
+  if (watch.joinable()) watch.join();
+  std::lock_guard<std::mutex> lk(p->mu);
+  DeviceGuard dg(p->local->device);
+  cudaStreamSynchronize(p->engine_stream);
+  cudaStreamDestroy(p->engine_stream);
+  cudaFreeHost(p->engine_ring);
+  cudaFreeHost(p->engine_done);
+  p->engine_stream = nullptr;
+  p->engine_ring = nullptr;
+  p->engine_done = nullptr;
+  p->engine_ctas = 0;
+  p->engine_quit = false;
+}
+
+// Lock NOT held.  ctas CTAs of kEngineThreads each, launched on demand.
+static kvd_status engine_configure(kvd_peer p, uint32_t ctas) {
+  engine_shutdown(p);
+  if (ctas == 0) return KVD_OK;
+  std::lock_guard<std::mutex> lk(p->mu);
+  if (p->row_bytes) return fail(KVD_EINVAL, "no engine on a head-sliced peer");
+  DeviceGuard dg(p->local->device);
+  if (!dg.ok) return fail(KVD_ECUDA, "cannot select device %d", p->local->device);
+  kvd::PullArgs a{};
+  kvd_status s = pair_args(p, kvd::kEngineTile, a);
+  if (s != KVD_OK) return s;
+  a.counter = p->counters;        // + slot, per request
+  a.flag = p->flags_dev;          // + slot
+  a.gt_out = p->gt_dev;           // + 4 * slot, timed requests
+  a.mbox = p->mbox;
+  p->engine_variant = aligned32(a, p->src_bases, p->local->bases) ? kvd::kLsu32 : kvd::kLsu16;
+  const size_t ring_bytes = (size_t)kvd::kEngineRing * kvd::kEngineLLWords * 8;
+  KVD_CUDA(cudaHostAlloc((void**)&p->engine_ring, ring_bytes,
+                         cudaHostAllocMapped | cudaHostAllocPortable));
+  memset(p->engine_ring, 0, ring_bytes);
+  KVD_CUDA(cudaHostAlloc((void**)&p->engine_done, kvd::kEngineRing * sizeof(unsigned long long),
+                         cudaHostAllocMapped | cudaHostAllocPortable));
+  memset(p->engine_done, 0, kvd::kEngineRing * sizeof(unsigned long long));
+  void* ring_dev = nullptr;
+  void* done_dev = nullptr;
+  KVD_CUDA(cudaHostGetDevicePointer(&ring_dev, p->engine_ring, 0));
+  KVD_CUDA(cudaHostGetDevicePointer(&done_dev, p->engine_done, 0));
+  KVD_CUDA(cudaStreamCreateWithFlags(&p->engine_stream, cudaStreamNonBlocking));
+  p->engine_params = kvd::EngineParams{};
+  p->engine_params.base = a;
+  p->engine_params.ll = (const unsigned long long*)ring_dev;
+  p->engine_params.done = (unsigned long long*)done_dev;
+  p->engine_tail = 0;
+  p->engine_live = false;
+  p->engine_ctas = ctas;
+  p->engine_quit = false;
+  p->engine_watch = std::thread([p] {
+    std::unique_lock<std::mutex> lk(p->mu);
+    while (!p->engine_quit) {
+      p->engine_cv.wait_for(lk, std::chrono::microseconds(500));
+      if (!p->engine_quit && p->engine_live &&
+          std::chrono::steady_clock::now() - p->engine_last > kEngineIdle)
+        engine_post_stop(p);
+    }
+  });
+  return KVD_OK;
+}
+
+// Post one request to the engine (pull, runs in p->runs).  false: take the
+// launch path (engine off, too big, too many runs, ring full).
+static bool engine_try_post(kvd_peer_s* p, const PairPlan& pp, uint32_t NL, uint64_t bytes,
+                            uint32_t slot, uint64_t token, uint64_t request_id,
+                            kvd_status* st) {
+  *st = KVD_OK;
+  if (!p->engine_ctas || bytes > kEngineMaxBytes || p->runs.empty() ||
+      p->runs.size() > kvd::kEngineMaxRuns || p->variant != KVD_VARIANT_AUTO ||
+      !engine_pos_free(p))
+    return false;
+  kvd::PullArgs t{};
+  *st = tile_runs(p->runs, pp, NL, kvd::kEngineTile, p->runs4, t);
+  if (*st != KVD_OK) return true;
+  const uint64_t mpos = p->mbox_next;
+  const uint32_t header[kvd::kEngineLLHeader] = {
+      (uint32_t)token, (uint32_t)(token >> 32), (uint32_t)request_id,
+      (uint32_t)(request_id >> 32), (uint32_t)mpos, (uint32_t)(mpos >> 32), slot, t.nruns,
+      t.tiles_per_lp, t.total_tiles, p->timing ? 1u : 0u, 0u};
+  DeviceGuard dg(p->local->device);
+  const cudaError_t e = dg.ok ? engine_ensure_live(p) : cudaErrorInvalidDevice;
+  if (e != cudaSuccess) {
+    *st = cuda_fail(e, "engine launch");
+    return true;
+  }
+  engine_publish(p, header, p->runs4.data(), t.nruns);
+  return true;
+}
+
 // Ring position of the next request's release post (issue order).
 static void mbox_commit(kvd_peer_s* p, uint64_t next) {
   p->mbox_next = next;
@@ -1600,6 +1802,31 @@ static kvd_status transfer(kvd_peer p, uint64_t request_id, const int32_t* src_i
   if (timed) {
     a.gt_start = p->gt_start + 2 * (size_t)slot;
     a.gt_out = p->gt_dev + 4 * (size_t)slot;
+  }
+
+  if (!push && !p->row_bytes && n > 0) {
+    kvd_status es;
+    if (engine_try_post(p, pp, NL, (uint64_t)n * NL * 2 * sg.span_bytes, slot, token,
+                        request_id, &es)) {
+      if (es != KVD_OK) return es;
+      kvd_pull_info info{};
+      info.request_id = request_id;
+      info.blocks = n;
+      info.runs = (uint32_t)p->runs.size();
+      info.bytes = (uint64_t)n * NL * 2 * sg.span_bytes;
+      info.segments = (uint64_t)NL * pp.planes * (pp.contiguous ? p->runs.size() : n);
+      info.tiles = p->runs4.empty() ? 0 : (uint64_t)p->runs4.back().w * NL * pp.planes;
+      info.ctas = p->engine_ctas;
+      info.threads = kvd::kEngineThreads;
+      info.variant = (uint32_t)(p->engine_variant == kvd::kLsu32 ? KVD_VARIANT_LSU32
+                                                                : KVD_VARIANT_LSU);
+      info.launches = 0;                   // posted to the resident engine
+      if (p->mbox) mbox_commit(p, p->mbox_next + 1);
+      cancel.armed = false;
+      slot_publish(p, slot, token, p->timing);
+      p->last = info;
+      return KVD_OK;
+    }
   }
 
   DeviceGuard dgd(p->local->device);
@@ -2003,6 +2230,7 @@ kvd_status kvd_peer_audit(kvd_peer p, uint64_t* violations) {
   if (!p->audit_ctr) return fail(KVD_ESTATE, "auditing is off (set KVD_OPT_AUDIT)");
   DeviceGuard dg(p->local->device);
   if (!dg.ok) return fail(KVD_ECUDA, "cannot select device %d", p->local->device);
+  engine_quiesce(p);
   KVD_CUDA(cudaDeviceSynchronize());
   unsigned int v = 0;
   KVD_CUDA(cudaMemcpy(&v, p->audit_ctr, sizeof(v), cudaMemcpyDeviceToHost));

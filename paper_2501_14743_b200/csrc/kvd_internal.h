@@ -124,6 +124,53 @@ struct PullArgs {
   unsigned long long* flags;        // per-slot completion words (pinned, host-mapped)
 };
 
+// Resident pull engine (KVD_OPT_ENGINE): a persistent kernel of a few CTAs
+// that drains a ring of request descriptors the host writes into pinned,
+// mapped memory -- the paper's transaction queue posted
+// straight to the device, so a short request costs neither a launch call nor
+// the launch latency.
+//
+// Ring entries use a low-latency ("LL") encoding: every 32-bit field is
+// stored as one 64-bit word {flag = low32(position + 1), value}, each word
+// single-copy atomic, so the engine validates an entry from the words it
+// read -- header and the first kEnginePollRuns runs in ONE PCIe round trip
+// of 16 B loads -- without a separate sequence word and a second read.
+// Word layout: [0,1] token, [2,3] request id, [4,5] mailbox position (lo,
+// hi), [6] slot, [7] nruns (kEngineStop: stop marker), [8] tiles per
+// (layer, plane), [9] total tiles, [10] flags (bit 0: timed), [11] pad,
+// then 4 words {src_start, dst_start, len, tile prefix} per run.
+constexpr unsigned int kEngineRing = 128;          // descriptors
+constexpr unsigned int kEngineMaxRuns = 64;        // larger tables take the launch path
+constexpr unsigned int kEngineTile = 2048;         // bytes per warp work item
+constexpr unsigned int kEngineThreads = 512;
+constexpr unsigned int kEngineMaxCtas = 8;         // one thread-block cluster (portable size)
+constexpr unsigned int kEngineLLHeader = 12;
+constexpr unsigned int kEngineLLWords = kEngineLLHeader + 4 * kEngineMaxRuns;
+constexpr unsigned int kEnginePollRuns = 8;
+// The plain descriptor CTA 0 of the engine's cluster writes into every CTA's
+// shared memory (distributed shared memory) once it validated an entry.
+struct alignas(16) EngineDesc {
+  unsigned long long token;
+  unsigned long long request_id;
+  unsigned long long mbox_pos;
+  unsigned long long t_seen;        // %globaltimer when CTA 0 validated the entry (timing)
+  unsigned int slot;
+  unsigned int nruns;
+  unsigned int tiles_per_lp;
+  unsigned int total_tiles;
+  unsigned int flags;
+  unsigned int pad[3];
+  int4 runs[kEngineMaxRuns];        // {src_start, dst_start, len, tile prefix}
+};
+constexpr unsigned int kEngineStop = 0xffffffffu;  // EngineDesc::nruns of a stop marker
+struct EngineParams {
+  PullArgs base;                    // request-independent fields (tiling, sides, slots)
+  const unsigned long long* ll;     // device pointer to the pinned ring [kEngineRing][LLWords]
+  unsigned long long first;         // ring position this launch starts at
+  unsigned long long* done;         // pinned [kEngineRing]: done[k % ring] = k + 1 once
+                                    // request k completed (its descriptor may be reused)
+};
+
 enum Variant : int { kLsu16 = 1, kLsu32 = 2, kTma = 4 };
 
 // Largest run table that travels inside the kernel parameters.
@@ -147,6 +194,12 @@ cudaError_t launch_pull(const PullArgs& args, const int4* runs_host, int variant
 cudaError_t launch_flag_only(unsigned long long* flag, unsigned long long token,
                              unsigned long long* mbox, unsigned long long mbox_pos,
                              unsigned long long request_id, cudaStream_t stream);
+
+// Launch the resident engine: ONE cluster of `ctas` (<= kEngineMaxCtas) CTAs
+// of kEngineThreads on `stream`; it runs until it reads a stop marker.
+// variant kLsu32 (32 B lanes) or kLsu16.
+cudaError_t launch_engine(const EngineParams& params, int variant, unsigned int ctas,
+                          cudaStream_t stream);
 
 // Resident CTAs per SM of the pull kernel for the given threads per CTA.
 int pull_ctas_per_sm(int variant, unsigned int threads, unsigned int nruns);

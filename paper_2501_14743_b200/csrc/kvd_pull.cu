@@ -26,6 +26,7 @@
 // float type ever touches the data): NaN payloads, -0, subnormals survive.
 // Pull kernels are launched with programmatic stream serialisation
 // (griddepcontrol): back-to-back pulls overlap launch with the previous tail.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -799,6 +800,162 @@ pull_kernel_tma_rows(const __grid_constant__ PullParams<MAXR> P, unsigned int st
   complete(a);
 }
 
+// ---------------------------------------------------------------------------
+// Resident pull engine (KVD_OPT_ENGINE): every CTA walks the descriptor ring
+// in order; for each request it takes its share of the tiles (one warp per
+// 2 KiB tile, grid-wide round robin), then arrives on the request's slot
+// counter -- the last CTA to arrive publishes the request exactly like a
+// launched pull (complete()).  Descriptors are read over PCIe from pinned
+// host memory: the sequence word with acquire, the rest with relaxed
+// system-scope loads, the run table by 64 threads at once.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void ld_relaxed_sys_v2(const unsigned long long* p, unsigned long long& x,
+                                                  unsigned long long& y) {
+  asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "l"(p) : "memory");
+}
+
+// The engine is ONE thread-block cluster.  CTA 0 is the leader: it polls the
+// pinned ring entry of request k (the header and the first kEnginePollRuns
+// runs, one 16 B LL chunk per thread, one PCIe round trip per poll),
+// validates it from the words' flags and writes the plain descriptor into
+// every CTA's shared memory (DSMEM).  A cluster barrier hands it over (the
+// other CTAs wait there in hardware, they never touch host memory); every
+// CTA copies its tiles, fences its stores, and a second cluster barrier
+// replaces the per-request arrival counter: after it CTA 0 publishes the
+// request with one system-scope release (cumulative over the other CTAs'
+// stores, ordered before it by the barrier's release/acquire).
+template <typename V, int U>
+__global__ void __launch_bounds__(kEngineThreads, 1)
+engine_kernel(const __grid_constant__ EngineParams E) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  __shared__ EngineDesc D;
+  __shared__ PullArgs A;
+  __shared__ unsigned long long ll[kEngineLLHeader + 4 * kEnginePollRuns];
+  __shared__ int go;
+  constexpr unsigned int kPoll = (kEngineLLHeader + 4 * kEnginePollRuns) / 2;   // chunks
+  constexpr unsigned int kPollers = 4;
+  static_assert(kPoll <= 32, "one poll = one warp of 16 B loads");
+  const unsigned int rank = cluster.block_rank();
+  const unsigned int ncta = cluster.num_blocks();
+  const unsigned int lane = threadIdx.x & 31u;
+  const unsigned int warps = blockDim.x >> 5;
+  const unsigned int gw = rank * warps + (threadIdx.x >> 5);
+  const unsigned int nw = ncta * warps;
+  for (unsigned long long k = E.first;; ++k) {
+    const unsigned int r = (unsigned int)(k % kEngineRing);
+    if (rank == 0) {
+      const unsigned long long* L = E.ll + (size_t)r * kEngineLLWords;
+      const unsigned long long want = (unsigned long long)(unsigned int)(k + 1);
+      // kPollers warps poll independently, staggered by a fraction of the
+      // PCIe round trip, so an entry is seen ~1 round trip after the host
+      // wrote it rather than ~1.5.  The first warp that validates it copies
+      // its words to shared memory.
+      const unsigned int w = threadIdx.x >> 5;
+      if (threadIdx.x == 0) go = 0;
+      __syncthreads();
+      if (w < kPollers) {
+        __nanosleep(w * 400);
+        for (;;) {
+          unsigned long long x = 0, y = 0;
+          if (lane < kPoll) ld_relaxed_sys_v2(L + 2 * lane, x, y);
+          // nruns is word 7 = chunk 3's second word
+          const unsigned int nr = (unsigned int)__shfl_sync(0xffffffffu, y, 3);
+          const unsigned int need = kEngineLLHeader +
+              (nr == kEngineStop ? 0u : 4u * min(nr, kEnginePollRuns));
+          const bool ok = lane >= kPoll ||
+                          ((2 * lane >= need || (x >> 32) == want) &&
+                           (2 * lane + 1 >= need || (y >> 32) == want));
+          const bool all = __all_sync(0xffffffffu, ok);
+          if (all && lane == 0 && atomicCAS(&go, 0, 1) == 0) go = 2 + (int)w;   // winner
+          __syncwarp();
+          const int g = *(volatile int*)&go;
+          if (g == 2 + (int)w && lane < kPoll) {
+            ll[2 * lane] = x;
+            ll[2 * lane + 1] = y;
+          }
+          if (g) break;
+        }
+      }
+      __syncthreads();
+      const unsigned long long t_seen = globaltimer();
+      const unsigned int nr = (unsigned int)ll[7];
+      // the descriptor, into every CTA's shared memory
+      for (unsigned int c = 0; c < ncta; ++c) {
+        EngineDesc* Dc = cluster.map_shared_rank(&D, c);
+        if (threadIdx.x == 0) {
+          Dc->token = (ll[0] & 0xffffffffull) | (ll[1] << 32);
+          Dc->request_id = (ll[2] & 0xffffffffull) | (ll[3] << 32);
+          Dc->mbox_pos = (ll[4] & 0xffffffffull) | (ll[5] << 32);
+          Dc->t_seen = t_seen;
+          Dc->slot = (unsigned int)ll[6];
+          Dc->nruns = nr;
+          Dc->tiles_per_lp = (unsigned int)ll[8];
+          Dc->total_tiles = (unsigned int)ll[9];
+          Dc->flags = (unsigned int)ll[10];
+        }
+      }
+      if (nr != kEngineStop) {
+        for (unsigned int q = threadIdx.x; q < 4 * nr; q += blockDim.x) {
+          unsigned long long w;
+          if (q < 4 * kEnginePollRuns) {
+            w = ll[kEngineLLHeader + q];
+          } else {                           // beyond the polled runs: wait for each word
+            do {
+              w = ld_relaxed_sys(L + kEngineLLHeader + q);
+            } while ((w >> 32) != want);
+          }
+          for (unsigned int c = 0; c < ncta; ++c)
+            reinterpret_cast<int*>(cluster.map_shared_rank(&D, c)->runs)[q] = (int)(unsigned int)w;
+        }
+      }
+    }
+    cluster.sync();                          // D is valid in every CTA
+    if (D.nruns == kEngineStop) return;
+    if (threadIdx.x == 0) {
+      A = E.base;
+      A.token = D.token;
+      A.request_id = D.request_id;
+      A.mbox_pos = D.mbox_pos;
+      A.nruns = D.nruns;
+      A.tiles_per_lp = D.tiles_per_lp;
+      A.total_tiles = D.total_tiles;
+      A.flag = E.base.flag + D.slot;
+      A.gt_out = (D.flags & 1u) ? E.base.gt_out + 4 * (size_t)D.slot : nullptr;
+    }
+    __syncthreads();
+    for (unsigned int t = gw; t < A.total_tiles; t += nw) {
+      const Tile T = tile_at(A, D.runs, t);
+      warp_copy<V, U>(T.dst, T.src, T.bytes, lane);
+    }
+    // every CTA's tiles landed: the barrier's cluster-scope release/acquire
+    // puts the other CTAs' stores before CTA 0's system-scope release in
+    // causality order (no per-thread gpu-scope fence needed)
+    cluster.sync();
+    if (rank == 0 && threadIdx.x == 0) {
+      if (A.gt_out != nullptr) {             // timed: CTA 0 saw the entry -> all tiles landed
+        const unsigned long long t1 = globaltimer();
+        volatile unsigned long long* o = A.gt_out;
+        o[0] = t1 - D.t_seen;
+        o[1] = D.t_seen;
+        o[2] = D.t_seen;
+        o[3] = t1;
+      }
+      publish_token(A, A.flag, A.token, A.request_id, A.mbox_pos);
+      asm volatile("st.relaxed.sys.global.u64 [%0], %1;" :: "l"(E.done + r), "l"(k + 1)
+                   : "memory");
+    }
+    // D and A are rewritten for the next request only after the next
+    // iteration's poll: every CTA has passed the barrier above by then
+  }
+}
+
 __global__ void flag_kernel(unsigned long long* flag, unsigned long long token,
                             unsigned long long* mbox, unsigned long long mbox_pos,
                             unsigned long long request_id) {
@@ -937,6 +1094,23 @@ cudaError_t launch_pull(const PullArgs& args, const int4* runs_host, int variant
   if (variant == kTma) return launch_tma(args, runs_host, ctas, threads, stages, stream);
   if (variant == kLsu32) return launch_v<V32, 4>(args, runs_host, ctas, threads, stream);
   return launch_v<V16, 8>(args, runs_host, ctas, threads, stream);
+}
+
+cudaError_t launch_engine(const EngineParams& params, int variant, unsigned int ctas,
+                          cudaStream_t stream) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ctas);
+  cfg.blockDim = dim3(kEngineThreads);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;   // the whole grid is one cluster
+  attr[0].val.clusterDim.x = ctas;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (variant == kLsu32) return cudaLaunchKernelEx(&cfg, engine_kernel<V32, 4>, params);
+  return cudaLaunchKernelEx(&cfg, engine_kernel<V16, 8>, params);
 }
 
 cudaError_t launch_flag_only(unsigned long long* flag, unsigned long long token,

@@ -22,7 +22,7 @@ FP16, BF16, FP8, FP32 = 0, 1, 2, 3
 VARIANT_AUTO, VARIANT_LSU, VARIANT_LSU32, VARIANT_CE, VARIANT_TMA = 0, 1, 2, 3, 4
 MEM_AUTO, MEM_POSIX_FD, MEM_FABRIC = 0, 1, 8
 OPT_MAX_CTAS, OPT_TILE_BYTES, OPT_COALESCE, OPT_VARIANT, OPT_THREADS, OPT_STAGES = 0, 1, 2, 3, 4, 5
-OPT_AUDIT, OPT_TIMING, OPT_STREAMS, OPT_EARLY_LOADS = 6, 7, 8, 9
+OPT_AUDIT, OPT_TIMING, OPT_STREAMS, OPT_EARLY_LOADS, OPT_ENGINE = 6, 7, 8, 9, 10
 
 EXPORTED = (
     "kvd_layout_geometry", "kvd_plan", "kvd_blob_info", "kvd_register_cache",

@@ -68,6 +68,7 @@ SCENARIOS = [
     ("batch_lsu32", "small", LSU32, "batch"),
     ("heads_auto", "shard0+shard1", AUTO, "heads"),
     ("heads_tma", "shard0+shard1", TMA, "heads"),
+    ("engine_short", "small", AUTO, "engine"),
 ]
 
 
@@ -148,6 +149,16 @@ def _scenario(kind, srcs, variant, blobs, dev, rid0):
                                        s, t)
             assert rc == oracle.OK, rc
 
+        if kind == "engine":                    # short requests through the resident engine
+            peers[0].set(kvd.OPT_ENGINE, 8)
+            for s, t in kvdgen.disjoint_fragmented_tables([3, 7, 1, 5, 6] * 4, sg.num_blocks,
+                                                          dg.num_blocks, 13):
+                rid += 1
+                peers[0].pull(rid, s, t)
+                assert peers[0].info()["launches"] == 0
+                peers[0].wait(rid)
+                done[names[0]].append(rid)
+                oracle_pull(names[0], s, t)
         if kind == "tables":
             for s, t in kvdgen.disjoint_fragmented_tables([100, 37, 64], sg.num_blocks,
                                                           dg.num_blocks, 8):

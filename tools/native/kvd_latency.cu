@@ -4,7 +4,7 @@
 //
 //   nvcc -O2 -I include tools/native/kvd_latency.cu -L paper_2501_14743_b200 -lkvd \
 //        -Xlinker -rpath=$PWD/paper_2501_14743_b200 -o tools/native/kvd_latency
-//   tools/native/kvd_latency [src_dev] [dst_dev] [iters] [timing 0|1]
+//   tools/native/kvd_latency [src_dev] [dst_dev] [iters] [timing 0|1] [engine CTAs]
 // timing 1 also reports the in-kernel %globaltimer span (KVD_OPT_TIMING = 2).
 #include <cuda_runtime.h>
 
@@ -47,7 +47,7 @@ static Cache make(int dev, const kvd_layout& L) {
 }
 
 static void run(const char* name, const kvd_layout& L, uint32_t n, int sdev, int ddev, int iters,
-                bool timing) {
+                bool timing, int engine) {
   Cache src = make(sdev, L), dst = make(ddev, L);
   std::vector<unsigned char> blob(1 << 16);
   size_t len = blob.size();
@@ -64,6 +64,7 @@ static void run(const char* name, const kvd_layout& L, uint32_t n, int sdev, int
   }
   std::vector<double> lat, call, span;
   if (timing) CK(kvd_peer_set(p, KVD_OPT_TIMING, 2));   // in-kernel %globaltimer spans
+  if (engine) CK(kvd_peer_set(p, KVD_OPT_ENGINE, engine));   // resident engine (short requests)
   for (int it = 0; it < iters + 20; ++it) {
     const uint64_t rid = 100 + it;
     auto t0 = std::chrono::steady_clock::now();
@@ -91,9 +92,10 @@ static void run(const char* name, const kvd_layout& L, uint32_t n, int sdev, int
   kvd_last_pull_info(p, &info);
   printf("{\"config\": \"%s\", \"src_dev\": %d, \"dst_dev\": %d, \"bytes\": %llu, \"variant\": %u, "
          "\"ctas\": %u, \"call_us_p50\": %.2f, \"latency_us_p50\": %.2f, \"latency_us_p90\": %.2f, "
-         "\"latency_us_min\": %.2f, \"kernel_span_us_p50\": %.2f, \"iters\": %d}\n",
+         "\"latency_us_min\": %.2f, \"kernel_span_us_p50\": %.2f, \"iters\": %d, \"engine\": %d, "
+         "\"launches\": %u}\n",
          name, sdev, ddev, (unsigned long long)info.bytes, info.variant, info.ctas, q(call, 0.5),
-         q(lat, 0.5), q(lat, 0.9), lat.front(), span.empty() ? -1.0 : q(span, 0.5), iters);
+         q(lat, 0.5), q(lat, 0.9), lat.front(), span.empty() ? -1.0 : q(span, 0.5), iters, engine, info.launches);
   kvd_close_peer(p);
   kvd_unregister_cache(dst.h);
   kvd_unregister_cache(src.h);
@@ -106,9 +108,10 @@ int main(int argc, char** argv) {
   const int ddev = argc > 2 ? atoi(argv[2]) : 0;
   const int iters = argc > 3 ? atoi(argv[3]) : 2000;
   const bool timing = argc > 4 && atoi(argv[4]) != 0;
+  const int engine = argc > 5 ? atoi(argv[5]) : 0;
   kvd_layout c1{2, 2, 64, 16, 64, KVD_FP16, {0, 0, 0, 0, 0}};
-  run("C1", c1, 16, sdev, ddev, iters, timing);
+  run("C1", c1, 16, sdev, ddev, iters, timing, engine);
   kvd_layout c2{32, 32, 128, 16, 1024, KVD_FP16, {0, 0, 0, 0, 0}};
-  run("C2", c2, 512, sdev, ddev, std::max(20, iters / 50), timing);
+  if (!engine) run("C2", c2, 512, sdev, ddev, std::max(20, iters / 50), timing, 0);
   return 0;
 }
