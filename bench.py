@@ -553,6 +553,8 @@ def run_kvd(args, rank, world, local_rank):
             peer.set(kvd.OPT_COALESCE, 0)
         if args.streams:
             peer.set(kvd.OPT_STREAMS, args.streams)
+        if args.early is not None:
+            peer.set(kvd.OPT_EARLY_LOADS, args.early)
 
     stream = torch.cuda.Stream(dev)
     rid = [rank * 10_000_000]
@@ -985,6 +987,8 @@ def main():
     ap.add_argument("--streams", type=int, default=0,
                     help="KVD_OPT_STREAMS: >= 2 lets consecutive pulls overlap on library "
                          "streams (completion still polled per request)")
+    ap.add_argument("--early", type=int, default=None,
+                    help="KVD_OPT_EARLY_LOADS (ring stages read before the preceding pull ends)")
     ap.add_argument("--memory", choices=["torch", "vmm"], default="torch",
                     help="cache memory: torch/cudaMalloc (legacy IPC) or kvd_mem_alloc (VMM, "
                          "POSIX-fd/fabric handles, §8 f3 groundwork)")

@@ -1890,6 +1890,11 @@ static kvd_status transfer(kvd_peer p, uint64_t request_id, const int32_t* src_i
     if (s != KVD_OK) return s;
     if (variant == KVD_VARIANT_TMA && !p->row_bytes) {
       a.tile_ctr = p->tile_ctrs + slot;
+      // claims of 2 tiles balance short requests best (10 MB: 456 -> 486
+      // GB/s back to back); long ones lose to the claim round trip under a
+      // saturated L2 and take 4 (C4 shard: 758 -> 778 GB/s,
+      // profiles/r02_claim_ab.jsonl)
+      a.claim = (uint64_t)a.total_tiles >= 128ull * ctas * (threads / 32) ? 4u : 2u;
       // the next pull's source reads overlap this one's tail
       a.early_loads = push ? 0u : p->early_loads;
     }

@@ -84,6 +84,7 @@ struct PullArgs {
   // which pipes claim tiles dynamically; reset by the last CTA.  nullptr:
   // static grid-stride order.
   unsigned int* tile_ctr;
+  unsigned int claim;               // tiles per dynamic claim (single pulls; 0: 4)
   // TMA single pulls over NVLink: lane 0 of each pipe claims and issues its
   // first early_loads ring stages of bulk loads from the SOURCE before
   // griddepcontrol.wait (0: none), so the ramp of a pull overlaps the drain

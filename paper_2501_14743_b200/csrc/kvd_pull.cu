@@ -610,7 +610,8 @@ pull_kernel_tma(const __grid_constant__ PullParams<MAXR> P, unsigned int stages)
     // it starts on the previous block), so a claim's round trip to L2 never
     // stalls the ring.
     constexpr unsigned int kNone = 0xffffffffu;
-    const unsigned int kClaim = a.nreqs ? K : 2u;   // batches: claim credit-friendly groups
+    // batches: credit-friendly groups; single pulls: the host's choice
+    const unsigned int kClaim = a.nreqs ? K : (a.claim ? a.claim : 4u);
     const unsigned int dealt = min(npipes * S, a.total_tiles);
     unsigned int handed = 0, cur = min(pipe * S, dealt), cur_end = min(pipe * S + S, dealt);
     unsigned int ahead = 0;
