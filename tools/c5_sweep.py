@@ -8,8 +8,13 @@ vs the NCCL N1 send/recv baseline on the same caches and block tables.
 
 One JSON line per point on rank 0.  Pull GB/s = bytes per pair / device time
 (CUDA events around the launch), aggregated as the sum over pairs / max time;
-NCCL = host wall per request (incl. the block-id message), max over ranks.
-Every point is parity-checked (fingerprints of the pulled blocks).
+NCCL = host wall per request (incl. the block-id message), max over ranks:
+N1 (whole request staged), N3 (double-buffered chunks, chunk size swept)
+and N0 (one contiguous message of the same bytes, NCCL's link ceiling);
+the pull is compared with the best paged-transfer variant.  Every point is
+parity-checked element by element (bench.decode_matches: the decode cache
+equals its regenerated pre-state with the pulled blocks replaced by the
+regenerated source blocks).
 """
 import argparse
 import json
@@ -21,7 +26,6 @@ import types
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -97,20 +101,15 @@ def main():
                                   "ctas": info.get("ctas"), "threads": info.get("threads")}
                 span = cache.span_bytes
                 per = n * NL * 2 * span
-
-                def fp(c, ids):
-                    idx = torch.from_numpy(np.ascontiguousarray(ids)).long().cuda(dev)
-                    w = torch.arange(1, span // 8 + 1, device=f"cuda:{dev}", dtype=torch.int64)
-                    return torch.stack([(c.layers[l].view(2, nb, -1)[:, idx].view(torch.int64) * w).sum(-1)
-                                        for l in range(NL)]).cpu()
-                fps = [None] * world
-                dist.all_gather_object(fps, fp(src, s_ids) if src else None, group=gloo)
-                ok = bool(torch.equal(fp(dst, d_ids), fps[me.peer])) if dst else True
+                # caches were filled with seed rank * 1000 + l: the source is
+                # the prefill rank's, the pre-state this rank's
+                ok = (bench.decode_matches(dst, g, s_ids, d_ids, me.peer, rank, dev)
+                      if dst else True)
                 base = {}
                 if not a.no_nccl:
                     args = types.SimpleNamespace(steps=a.iters, no_n2=True)
                     base = bench.nccl_baselines(args, g, [(s_ids, d_ids)], src, dst, me.role, rank, half,
-                                                dev, gloo, fp)
+                                                dev, gloo, me.peer)
                 stats = {"res": res, "ok": ok, "base": base, "bytes": per if dst else 0}
                 all_s = cluster.gather_stats(stats, gloo)
                 if rank == 0:
@@ -126,12 +125,20 @@ def main():
                     out["threads"] = dec[0]["res"]["pull"].get("threads")
                     out["ctas"] = dec[0]["res"]["pull"]["ctas"]
                     if not a.no_nccl:
-                        rs = [s["base"]["n1_gather_send_recv_scatter"] for s in dec]
-                        t = max(x["wall_s"] for x in rs)
-                        out["nccl_n1_gbs_per_pair"] = round(per * rs[0]["steps"] / t / 1e9, 1)
-                        out["nccl_parity"] = all(s["base"]["n1_gather_send_recv_scatter"]["ok"]
-                                                 for s in all_s if s["base"])
-                        out["pull_vs_nccl"] = round(out["pull_gbs_per_pair"] / out["nccl_n1_gbs_per_pair"], 2)
+                        nccl = {}
+                        for name in dec[0]["base"]:
+                            rs = [s["base"][name] for s in dec]
+                            t = max(x["wall_s"] for x in rs)
+                            nccl[name] = round(per * rs[0]["steps"] / t / 1e9, 1)
+                        out["nccl_gbs_per_pair"] = nccl
+                        out["nccl_parity"] = all(v["ok"] for s in all_s if s["base"]
+                                                 for v in s["base"].values())
+                        transfers = {k: v for k, v in nccl.items() if not k.startswith("n0")}
+                        best = max(transfers, key=transfers.get)
+                        out["nccl_best_transfer"] = best
+                        out["pull_vs_best_nccl"] = round(out["pull_gbs_per_pair"] / transfers[best], 2)
+                        out["pull_vs_nccl_n0_ceiling"] = round(
+                            out["pull_gbs_per_pair"] / nccl["n0_raw_contiguous"], 2)
                     out["parity"] = all(s["ok"] for s in all_s)
                     print(json.dumps(out), flush=True)
                 if peer:

@@ -81,7 +81,9 @@ def main():
     cfgs = [(f"tma{c}" if len(tma_ctas) > 1 else "tma",
              {kvd.OPT_VARIANT: kvd.VARIANT_TMA, kvd.OPT_THREADS: 32, kvd.OPT_STAGES: 6,
               kvd.OPT_TILE_BYTES: 32768, kvd.OPT_MAX_CTAS: c}) for c in tma_ctas]
-    for name, opts in (*cfgs,
+    # "auto" first: the library's own launch policy (later configs set
+    # options that stay set on the peer)
+    for name, opts in (("auto", {}), *cfgs,
                        ("lsu", {kvd.OPT_VARIANT: kvd.VARIANT_LSU32, kvd.OPT_THREADS: 512,
                                 kvd.OPT_TILE_BYTES: 16384, kvd.OPT_MAX_CTAS: 0}),
                        ("ce", {kvd.OPT_VARIANT: kvd.VARIANT_CE})):
