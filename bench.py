@@ -756,6 +756,14 @@ def run_kvd(args, rank, world, local_rank):
         ce_gbs = timed_contiguous()
         peer.set(kvd.OPT_VARIANT, {"lsu": 1, "lsu32": 2, "ce": 3, "tma": 4}.get(args.variant, 0))
         tma_gbs = timed_contiguous()
+    # The measured link ceiling (SURVEY §8 d, the calibration kernel): pure
+    # bulk reads of the prefill cache through the same mapping, no stores
+    # (kvd_peer_calibrate), best over grid sizes; the NVLink roofline's peak.
+    read_ceiling = None
+    if peer and multi and args.config != "c1":
+        nbytes = min(g.num_layers * (dst.layer_bytes // 32768) * 32768, 2 << 30)
+        read_ceiling = {f"{c}x{st}": peer.calibrate(nbytes, ctas=c, stages=st, reps=3)
+                        for c in (48, 96, 148) for st in (6, 7)}
 
     base = {}
     if multi and not args.no_nccl:
@@ -773,7 +781,8 @@ def run_kvd(args, rank, world, local_rank):
              "gt_ms_total": gt_ms_total, "gt_launches": gt_launches,
              "lat": lat_ns, "clock": sampler.summary(), "info": info, "base": base,
              "launches": timed_launches, "runs": info.get("runs"), "ce_gbs": ce_gbs,
-             "tma_gbs": tma_gbs, "lat_queued": lat_queued, "lat_engine": lat_engine,
+             "tma_gbs": tma_gbs, "read_ceiling": read_ceiling,
+             "lat_queued": lat_queued, "lat_engine": lat_engine,
              "bytes_per_step": bytes_per_step if peer else 0}
     all_stats = cluster.gather_stats(stats, gloo) if multi else [stats]
 
@@ -799,13 +808,26 @@ def run_kvd(args, rank, world, local_rank):
         achieved_link = float(np.mean(per_pair))
         bytes_per_step = dec[0]["bytes_per_step"]
         if multi:
-            peak = NVLINK_READ_USER_GBS
+            ceil = [max(s["read_ceiling"].values()) for s in dec if s["read_ceiling"]]
+            measured = float(np.mean(ceil)) if len(ceil) == len(dec) else None
+            peak = measured or NVLINK_READ_USER_GBS
             roof = {"bound": "nvlink", "achieved": round(achieved_link, 1),
                     "peak": round(peak, 1), "unit": "GB/s",
                     "frac": round(achieved_link / peak, 4),
-                    "peak_source": "NVLink 5 read user-data ceiling: 900 GB/s per direction x "
-                                   "128/144 (16 B protocol per 128 B read response, measured by "
-                                   "the ncu nvlrx counters in nvlink_rx)",
+                    "peak_source": ("measured in this run: kvd_peer_calibrate, discarded bulk "
+                                    "(TMA) reads of the prefill cache through the same NVLink "
+                                    "mapping, no stores, best of 48/96/148 CTAs x 6/7 stages of 32 KiB, "
+                                    "mean over pairs"
+                                    if measured else
+                                    "NVLink 5 read user-data ceiling: 900 GB/s per direction x "
+                                    "128/144 (16 B protocol per 128 B read response, measured by "
+                                    "the ncu nvlrx counters in nvlink_rx)"),
+                    "measured_read_ceiling": ({"per_pair": [{str(k): round(v, 1) for k, v in
+                                                             s["read_ceiling"].items()}
+                                                            for s in dec],
+                                               "what": "GB/s by CTAs x ring stages"}
+                                              if measured else None),
+                    "frac_of_read_user_ceiling_800": round(achieved_link / NVLINK_READ_USER_GBS, 4),
                     "frac_of_guide_770": round(achieved_link / NVLINK_MEASURED_GBS, 4),
                     "frac_of_nominal_900": round(achieved_link / NVLINK_NOMINAL_GBS, 4),
                     "algorithmic_bytes_per_step": bytes_per_step,

@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define KVD_ABI_VERSION 2
+#define KVD_ABI_VERSION 3
 
 #if defined(__GNUC__)
 #define KVD_API __attribute__((visibility("default")))
@@ -172,13 +172,13 @@ typedef enum {
                                work queued earlier on the same stream (in the paper's flow they
                                are the prefill worker's finished cache, written by another
                                process).  0: every access waits (strict stream order) */
-  KVD_OPT_ENGINE = 10       /* c in [0, 8], default 0 (off): the resident pull engine for short
+  KVD_OPT_ENGINE = 10       /* c in [0, 16], default 0 (off): the resident pull engine for short
                                requests -- one thread-block cluster of c CTAs (a persistent
-                               kernel) drains a ring of request descriptors the host writes
-                               into pinned memory (the paper's
-                               transaction queue, posted straight to the device), so
-                               a kvd_pull of <= 2 MiB in <= 64 runs (AUTO variant, not head-
-                               sliced) makes no CUDA call and pays no launch latency.  The
+                               kernel; c > 8 is a non-portable cluster size B200 allows)
+                               drains a ring of request descriptors the host writes into
+                               pinned memory (the paper's transaction queue, P:L373-378,
+                               posted straight to the device), so a kvd_pull of <= 2 MiB in
+                               <= 64 runs (AUTO variant, not head-sliced) makes no CUDA call and pays no launch latency.  The
                                engine is launched on the first such request and exits after
                                2 ms without one (a watchdog thread), so it holds c SMs only
                                while short requests flow.  Such requests are NOT ordered with
@@ -443,6 +443,23 @@ typedef struct {
  * poller) since the previous call, oldest first, at most `cap` (and at most
  * the 4096 most recent); *n = how many were written. */
 KVD_API kvd_status kvd_peer_spans(kvd_peer peer, kvd_span* out, uint32_t cap, uint32_t* n);
+
+/* Link calibration (SURVEY.md §8 d: GB/s "as a fraction of the measured
+ * achievable link ceiling (calibration kernel)"): reads `bytes` of the
+ * peer's SOURCE cache memory -- layer after layer from each layer's base,
+ * contiguous 32 KiB chunks, no block table -- with bulk (TMA) loads into
+ * shared memory that are discarded (no stores), `reps` times back to back,
+ * and returns bytes * reps / device time (CUDA events) in GB/s (1e9 B/s).
+ * That is the most this GPU's SMs can read through the mapping (over NVLink
+ * for a peer on another GPU), the ceiling a pull can approach.  `ctas` CTAs
+ * of one `stages`-deep ring each (0: one per SM; stages 0: 6).  Synchronous
+ * (runs on an internal stream, waits for it); takes the peer lock; a
+ * measurement tool, not part of the transfer path.
+ * Errors: KVD_EINVAL (null gbs, reps 0, stages > 7 -- 7 x 32 KiB fill the
+ * shared memory -- or bytes < 32 KiB),
+ * KVD_ERANGE (bytes more than the source layers hold), KVD_ECUDA. */
+KVD_API kvd_status kvd_peer_calibrate(kvd_peer peer, uint64_t bytes, uint32_t ctas,
+                                      uint32_t stages, uint32_t reps, double* gbs);
 
 /* Describe the most recent kvd_pull on this peer. */
 KVD_API kvd_status kvd_last_pull_info(kvd_peer peer, kvd_pull_info* out);

@@ -144,7 +144,7 @@ constexpr unsigned int kEngineRing = 128;          // descriptors
 constexpr unsigned int kEngineMaxRuns = 64;        // larger tables take the launch path
 constexpr unsigned int kEngineTile = 2048;         // bytes per warp work item
 constexpr unsigned int kEngineThreads = 512;
-constexpr unsigned int kEngineMaxCtas = 8;         // one thread-block cluster (portable size)
+constexpr unsigned int kEngineMaxCtas = 16;        // one thread-block cluster (> 8: non-portable)
 constexpr unsigned int kEngineLLHeader = 12;
 constexpr unsigned int kEngineLLWords = kEngineLLHeader + 4 * kEngineMaxRuns;
 constexpr unsigned int kEnginePollRuns = 8;
@@ -201,6 +201,16 @@ cudaError_t launch_flag_only(unsigned long long* flag, unsigned long long token,
 // variant kLsu32 (32 B lanes) or kLsu16.
 cudaError_t launch_engine(const EngineParams& params, int variant, unsigned int ctas,
                           cudaStream_t stream);
+
+// Link calibration (kvd_peer_calibrate): `ctas` CTAs each run an
+// `stages`-deep ring of kCalibChunk bulk loads over total_chunks chunks of
+// the layers at bases[] (device array; layer_chunks chunks per layer) and
+// discard them.  stages in [1, kCalibMaxStages].
+constexpr unsigned int kCalibChunk = 32768;
+constexpr unsigned int kCalibMaxStages = 7;   // 224 KiB of shared memory
+cudaError_t launch_calib_read(const unsigned long long* bases, unsigned long long layer_chunks,
+                              unsigned long long total_chunks, unsigned int ctas,
+                              unsigned int stages, cudaStream_t stream);
 
 // Resident CTAs per SM of the pull kernel for the given threads per CTA.
 int pull_ctas_per_sm(int variant, unsigned int threads, unsigned int nruns);

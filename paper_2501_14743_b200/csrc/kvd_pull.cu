@@ -849,6 +849,8 @@ engine_kernel(const __grid_constant__ EngineParams E) {
   const unsigned int warps = blockDim.x >> 5;
   const unsigned int gw = rank * warps + (threadIdx.x >> 5);
   const unsigned int nw = ncta * warps;
+  // the request-independent fields once; per request only the few below
+  if (threadIdx.x == 0) A = E.base;
   for (unsigned long long k = E.first;; ++k) {
     const unsigned int r = (unsigned int)(k % kEngineRing);
     if (rank == 0) {
@@ -919,8 +921,8 @@ engine_kernel(const __grid_constant__ EngineParams E) {
     }
     cluster.sync();                          // D is valid in every CTA
     if (D.nruns == kEngineStop) return;
+    const unsigned long long t_handed = globaltimer();   // timing: descriptor in every CTA
     if (threadIdx.x == 0) {
-      A = E.base;
       A.token = D.token;
       A.request_id = D.request_id;
       A.mbox_pos = D.mbox_pos;
@@ -945,7 +947,7 @@ engine_kernel(const __grid_constant__ EngineParams E) {
         volatile unsigned long long* o = A.gt_out;
         o[0] = t1 - D.t_seen;
         o[1] = D.t_seen;
-        o[2] = D.t_seen;
+        o[2] = t_handed;                     // the span's "wait": descriptor handed over
         o[3] = t1;
       }
       publish_token(A, A.flag, A.token, A.request_id, A.mbox_pos);
@@ -954,6 +956,42 @@ engine_kernel(const __grid_constant__ EngineParams E) {
     }
     // D and A are rewritten for the next request only after the next
     // iteration's poll: every CTA has passed the barrier above by then
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Link calibration (kvd_peer_calibrate, SURVEY.md §8 d "fraction of the
+// measured achievable link ceiling"): pure ingress.  One elected lane per
+// CTA runs an S-stage ring of kCalibChunk bulk loads from the peer-mapped
+// source layers into shared memory and discards them -- no stores, no block
+// table, no completion -- so the rate is what this GPU's SMs can pull from
+// the mapping at all.  Chunk i of the request is byte (i % layer_chunks) *
+// kCalibChunk of layer i / layer_chunks; CTA c takes chunks c, c + G, ...
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(32)
+calib_read_kernel(const unsigned long long* __restrict__ bases, unsigned long long layer_chunks,
+                  unsigned long long total_chunks, unsigned int stages) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ uint64_t bar[kMaxStages];
+  if (threadIdx.x != 0) return;
+  for (unsigned int s = 0; s < stages; ++s) mbar_init(&bar[s]);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  auto src = [&](unsigned long long i) {
+    return reinterpret_cast<const char*>(bases[i / layer_chunks] + (i % layer_chunks) * kCalibChunk);
+  };
+  unsigned long long next = blockIdx.x;
+  unsigned int issued = 0;
+  for (unsigned int s = 0; s < stages && next < total_chunks; ++s, next += gridDim.x, ++issued)
+    tma_load(smem + (size_t)s * kCalibChunk, src(next), kCalibChunk, &bar[s]);
+  for (unsigned int i = 0; i < issued; ++i) {
+    const unsigned int s = i % stages;
+    mbar_wait(&bar[s], (i / stages) & 1u);
+    // the stage was written by the async proxy and never read: refill at once
+    if (next < total_chunks) {
+      tma_load(smem + (size_t)s * kCalibChunk, src(next), kCalibChunk, &bar[s]);
+      next += gridDim.x;
+      ++issued;
+    }
   }
 }
 
@@ -1110,14 +1148,29 @@ cudaError_t launch_engine(const EngineParams& params, int variant, unsigned int 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (variant == kLsu32) return cudaLaunchKernelEx(&cfg, engine_kernel<V32, 4>, params);
-  return cudaLaunchKernelEx(&cfg, engine_kernel<V16, 8>, params);
+  auto kernel = variant == kLsu32 ? engine_kernel<V32, 4> : engine_kernel<V16, 8>;
+  if (ctas > 8) {   // 16: a non-portable cluster size (B200 allows it on request)
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaLaunchKernelEx(&cfg, kernel, params);
 }
 
 cudaError_t launch_flag_only(unsigned long long* flag, unsigned long long token,
                              unsigned long long* mbox, unsigned long long mbox_pos,
                              unsigned long long request_id, cudaStream_t stream) {
   flag_kernel<<<1, 1, 0, stream>>>(flag, token, mbox, mbox_pos, request_id);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_calib_read(const unsigned long long* bases, unsigned long long layer_chunks,
+                              unsigned long long total_chunks, unsigned int ctas,
+                              unsigned int stages, cudaStream_t stream) {
+  const size_t smem = (size_t)stages * kCalibChunk;
+  cudaError_t e = cudaFuncSetAttribute(calib_read_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  calib_read_kernel<<<ctas, 32, smem, stream>>>(bases, layer_chunks, total_chunks, stages);
   return cudaGetLastError();
 }
 

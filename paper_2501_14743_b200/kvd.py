@@ -32,7 +32,7 @@ EXPORTED = (
     "kvd_peer_set", "kvd_pull", "kvd_push", "kvd_pull_batch", "kvd_poll_done", "kvd_wait_done",
     "kvd_poll_many",
     "kvd_last_pull_info", "kvd_peer_audit", "kvd_peer_kernel_time", "kvd_peer_device_time",
-    "kvd_peer_spans",
+    "kvd_peer_spans", "kvd_peer_calibrate",
     "kvd_stream_wait",
     "kvd_poll_released",
     "kvd_gather", "kvd_scatter", "kvd_strerror", "kvd_last_error", "kvd_abi_version",
@@ -88,7 +88,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 
 # The ABI version is checked before any other symbol is bound, so a stale
 # library fails here with a clear message rather than with AttributeError.
-ABI_VERSION = 2     # include/kvd.h KVD_ABI_VERSION this binding was written against
+ABI_VERSION = 3     # include/kvd.h KVD_ABI_VERSION this binding was written against
 _lib.kvd_abi_version.argtypes = []
 _lib.kvd_abi_version.restype = ctypes.c_int
 if _lib.kvd_abi_version() != ABI_VERSION:
@@ -129,6 +129,7 @@ _SIGS = {
     "kvd_peer_kernel_time": [_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_u64)],
     "kvd_peer_device_time": [_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_u64)],
     "kvd_peer_spans": [_p, _p, _u32, ctypes.POINTER(_u32)],
+    "kvd_peer_calibrate": [_p, _u64, _u32, _u32, _u32, ctypes.POINTER(ctypes.c_double)],
     "kvd_stream_wait": [_p, _p],
     "kvd_gather": [_p, _pi32, _u32, _p, _p],
     "kvd_scatter": [_p, _pi32, _u32, _p, _p],
@@ -386,6 +387,16 @@ def kvd_peer_spans(peer: int, cap: int = 4096) -> list:
     _check(_lib.kvd_peer_spans(peer, ctypes.cast(buf, _p), cap, ctypes.byref(n)), "kvd_peer_spans")
     return [(buf[i].request_id, buf[i].start_ns, buf[i].wait_ns, buf[i].end_ns)
             for i in range(n.value)]
+
+
+def kvd_peer_calibrate(peer: int, nbytes: int, ctas: int = 0, stages: int = 0,
+                       reps: int = 3) -> float:
+    """Measured link ceiling: GB/s of discarded bulk reads of `nbytes` of the
+    peer's source layers (no stores, no block table), `reps` launches."""
+    g = ctypes.c_double(0)
+    _check(_lib.kvd_peer_calibrate(peer, int(nbytes), int(ctas), int(stages), int(reps),
+                                   ctypes.byref(g)), "kvd_peer_calibrate")
+    return g.value
 
 
 def kvd_stream_wait(peer: int, stream: int) -> None:

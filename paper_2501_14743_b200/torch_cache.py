@@ -155,6 +155,11 @@ class Peer:
         retired single pulls since the last call; needs OPT_TIMING."""
         return kvd.kvd_peer_device_time(self.handle)
 
+    def calibrate(self, nbytes: int, ctas: int = 0, stages: int = 0, reps: int = 3) -> float:
+        """Measured link ceiling (GB/s): discarded bulk reads of `nbytes` of the
+        peer's source layers, no stores (kvd_peer_calibrate)."""
+        return kvd.kvd_peer_calibrate(self.handle, nbytes, ctas, stages, reps)
+
     def spans(self) -> list:
         """[(request_id, start_ns, wait_ns, end_ns)] %globaltimer timelines of the
         timed single pulls retired since the last call; needs OPT_TIMING."""

@@ -48,7 +48,7 @@ def test_library_exports_every_declared_symbol(kvd):
     assert declared <= exported, declared - exported
     assert exported <= declared, exported - declared       # nothing undeclared leaks
     assert set(kvd.EXPORTED) == declared
-    assert kvd.kvd_abi_version() == 2
+    assert kvd.kvd_abi_version() == 3
 
 
 def test_library_has_no_libcudart_or_torch_dependency(kvd):

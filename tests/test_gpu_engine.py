@@ -24,12 +24,12 @@ def _engine_pair(seed, ctas=8, g=G):
     return pair
 
 
-@pytest.mark.parametrize("ctas", [1, 3, 8])
+@pytest.mark.parametrize("ctas", [1, 3, 8, 16])
 def test_engine_small_pulls_bit_exact(ctas):
     pair = _engine_pair(90 + ctas, ctas)
     try:
         with pytest.raises(kvd.KvdError):
-            pair.peer.set(kvd.OPT_ENGINE, 9)              # one cluster: at most 8 CTAs
+            pair.peer.set(kvd.OPT_ENGINE, 17)             # one cluster: at most 16 CTAs
         rng = np.random.default_rng(ctas)
         exp = pair.dst_host
         for it in range(60):

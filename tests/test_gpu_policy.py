@@ -92,3 +92,46 @@ def test_device_time_globaltimer_cross_check():
         assert_layers_equal(pair.download_dst(), pair.expected(s, d))
     finally:
         pair.close()
+
+
+def test_link_calibration_reads_only():
+    """kvd_peer_calibrate (SURVEY §8 d, the measured link ceiling): pure bulk
+    reads of the source layers.  Loopback reads local HBM (no write traffic,
+    so above the HBM copy rate's read half); errors on bad sizes; and it
+    leaves both caches untouched."""
+    from paper_2501_14743_b200 import kvd
+    pair = make_pair(G7B, G7B, seed=106)
+    try:
+        before_src = [t.clone() for t in pair.src.layers]
+        before_dst = [t.clone() for t in pair.dst.layers]
+        total = G7B.num_layers * pair.src.layer_bytes
+        gbs = pair.peer.calibrate(min(total, 1 << 30), reps=2)
+        assert 1000 < gbs < 9000, gbs
+        with pytest.raises(kvd.KvdError) as e:
+            pair.peer.calibrate(1024)
+        assert e.value.status == kvd.EINVAL
+        with pytest.raises(kvd.KvdError) as e:
+            pair.peer.calibrate(total + (1 << 20))
+        assert e.value.status == kvd.ERANGE
+        with pytest.raises(kvd.KvdError) as e:
+            pair.peer.calibrate(1 << 20, stages=8)
+        assert e.value.status == kvd.EINVAL
+        torch.cuda.synchronize()
+        for a, b in zip(before_src, pair.src.layers):
+            assert torch.equal(a, b)
+        for a, b in zip(before_dst, pair.dst.layers):
+            assert torch.equal(a, b)
+    finally:
+        pair.close()
+
+
+def test_link_calibration_over_nvlink():
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs")
+    pair = make_pair(G7B, G7B, seed=107, src_dev=0, dst_dev=1)
+    try:
+        total = G7B.num_layers * (pair.src.layer_bytes // 32768) * 32768
+        gbs = max(pair.peer.calibrate(total, ctas=c, reps=2) for c in (48, 148))
+        assert 600 < gbs < 900, gbs      # NVLink 5: 900 GB/s per direction on the wire
+    finally:
+        pair.close()

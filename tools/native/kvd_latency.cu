@@ -12,6 +12,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "kvd.h"
@@ -62,8 +63,20 @@ static void run(const char* name, const kvd_layout& L, uint32_t n, int sdev, int
     si[i] = (int32_t)(2 * i % L.num_blocks);
     di[i] = (int32_t)((2 * i + 1) % L.num_blocks);
   }
-  std::vector<double> lat, call, span;
+  std::vector<double> lat, call, span, pre;
   if (timing) CK(kvd_peer_set(p, KVD_OPT_TIMING, 2));   // in-kernel %globaltimer spans
+  // KVD_LAT_OPTS="option=value,...": extra kvd_peer_set calls (e.g. "0=16,4=256"
+  // for 16 CTAs of 256 threads) to sweep the small-request launch shape
+  if (const char* o = getenv("KVD_LAT_OPTS")) {
+    int opt = 0;
+    long long val = 0;
+    for (const char* q = o; sscanf(q, "%d=%lld", &opt, &val) == 2;) {
+      CK(kvd_peer_set(p, opt, val));
+      q = strchr(q, ',');
+      if (!q) break;
+      ++q;
+    }
+  }
   if (engine) CK(kvd_peer_set(p, KVD_OPT_ENGINE, engine));   // resident engine (short requests)
   for (int it = 0; it < iters + 20; ++it) {
     const uint64_t rid = 100 + it;
@@ -81,10 +94,14 @@ static void run(const char* name, const kvd_layout& L, uint32_t n, int sdev, int
       kvd_span sp;
       uint32_t k = 0;
       CK(kvd_peer_spans(p, &sp, 1, &k));
-      if (k && it >= 20) span.push_back((sp.end_ns - sp.start_ns) * 1e-3);
+      if (k && it >= 20) {
+        span.push_back((sp.end_ns - sp.start_ns) * 1e-3);
+        pre.push_back((sp.wait_ns - sp.start_ns) * 1e-3);   // engine: entry seen -> handed over
+      }
     }
   }
   std::sort(span.begin(), span.end());
+  std::sort(pre.begin(), pre.end());
   std::sort(lat.begin(), lat.end());
   std::sort(call.begin(), call.end());
   auto q = [](const std::vector<double>& v, double f) { return v[(size_t)(f * (v.size() - 1))]; };
@@ -92,10 +109,10 @@ static void run(const char* name, const kvd_layout& L, uint32_t n, int sdev, int
   kvd_last_pull_info(p, &info);
   printf("{\"config\": \"%s\", \"src_dev\": %d, \"dst_dev\": %d, \"bytes\": %llu, \"variant\": %u, "
          "\"ctas\": %u, \"call_us_p50\": %.2f, \"latency_us_p50\": %.2f, \"latency_us_p90\": %.2f, "
-         "\"latency_us_min\": %.2f, \"kernel_span_us_p50\": %.2f, \"iters\": %d, \"engine\": %d, "
-         "\"launches\": %u}\n",
+         "\"latency_us_min\": %.2f, \"kernel_span_us_p50\": %.2f, \"pre_us_p50\": %.2f, \"iters\": %d, \"engine\": %d, "
+         "\"launches\": %u, \"threads\": %u, \"opts\": \"%s\"}\n",
          name, sdev, ddev, (unsigned long long)info.bytes, info.variant, info.ctas, q(call, 0.5),
-         q(lat, 0.5), q(lat, 0.9), lat.front(), span.empty() ? -1.0 : q(span, 0.5), iters, engine, info.launches);
+         q(lat, 0.5), q(lat, 0.9), lat.front(), span.empty() ? -1.0 : q(span, 0.5), pre.empty() ? -1.0 : q(pre, 0.5), iters, engine, info.launches, info.threads, getenv("KVD_LAT_OPTS") ? getenv("KVD_LAT_OPTS") : "");
   kvd_close_peer(p);
   kvd_unregister_cache(dst.h);
   kvd_unregister_cache(src.h);
@@ -112,6 +129,7 @@ int main(int argc, char** argv) {
   kvd_layout c1{2, 2, 64, 16, 64, KVD_FP16, {0, 0, 0, 0, 0}};
   run("C1", c1, 16, sdev, ddev, iters, timing, engine);
   kvd_layout c2{32, 32, 128, 16, 1024, KVD_FP16, {0, 0, 0, 0, 0}};
-  if (!engine) run("C2", c2, 512, sdev, ddev, std::max(20, iters / 50), timing, 0);
+  if (!engine && !getenv("KVD_LAT_C1_ONLY"))
+    run("C2", c2, 512, sdev, ddev, std::max(20, iters / 50), timing, 0);
   return 0;
 }
