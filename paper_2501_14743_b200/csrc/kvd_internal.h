@@ -147,23 +147,11 @@ constexpr unsigned int kEngineThreads = 512;
 constexpr unsigned int kEngineMaxCtas = 16;        // one thread-block cluster (> 8: non-portable)
 constexpr unsigned int kEngineLLHeader = 12;
 constexpr unsigned int kEngineLLWords = kEngineLLHeader + 4 * kEngineMaxRuns;
-constexpr unsigned int kEnginePollRuns = 8;
-// The plain descriptor CTA 0 of the engine's cluster writes into every CTA's
-// shared memory (distributed shared memory) once it validated an entry.
-struct alignas(16) EngineDesc {
-  unsigned long long token;
-  unsigned long long request_id;
-  unsigned long long mbox_pos;
-  unsigned long long t_seen;        // %globaltimer when CTA 0 validated the entry (timing)
-  unsigned int slot;
-  unsigned int nruns;
-  unsigned int tiles_per_lp;
-  unsigned int total_tiles;
-  unsigned int flags;
-  unsigned int pad[3];
-  int4 runs[kEngineMaxRuns];        // {src_start, dst_start, len, tile prefix}
-};
-constexpr unsigned int kEngineStop = 0xffffffffu;  // EngineDesc::nruns of a stop marker
+// one poll reads the header and this many runs (two 16 B loads per lane):
+// fragmented short requests rarely have more, and more words would cost a
+// second PCIe round trip (C1 with 16 runs: entry seen -> handed over 1.7 us)
+constexpr unsigned int kEnginePollRuns = 16;
+constexpr unsigned int kEngineStop = 0xffffffffu;  // nruns of a stop marker
 struct EngineParams {
   PullArgs base;                    // request-independent fields (tiling, sides, slots)
   const unsigned long long* ll;     // device pointer to the pinned ring [kEngineRing][LLWords]

@@ -823,9 +823,10 @@ __device__ __forceinline__ void ld_relaxed_sys_v2(const unsigned long long* p, u
 
 // The engine is ONE thread-block cluster.  CTA 0 is the leader: it polls the
 // pinned ring entry of request k (the header and the first kEnginePollRuns
-// runs, one 16 B LL chunk per thread, one PCIe round trip per poll),
-// validates it from the words' flags and writes the plain descriptor into
-// every CTA's shared memory (DSMEM).  A cluster barrier hands it over (the
+// runs, 16 B LL chunks, one PCIe round trip per poll), validates it from the
+// words' flags and writes the per-request fields and the run table into
+// every CTA's shared memory (DSMEM, one remote store per thread in
+// parallel).  A cluster barrier hands it over (the
 // other CTAs wait there in hardware, they never touch host memory); every
 // CTA copies its tiles, fences its stores, and a second cluster barrier
 // replaces the per-request arrival counter: after it CTA 0 publishes the
@@ -836,105 +837,117 @@ __global__ void __launch_bounds__(kEngineThreads, 1)
 engine_kernel(const __grid_constant__ EngineParams E) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
-  __shared__ EngineDesc D;
-  __shared__ PullArgs A;
-  __shared__ unsigned long long ll[kEngineLLHeader + 4 * kEnginePollRuns];
+  __shared__ int4 runs[kEngineMaxRuns];    // this request's run table (written by CTA 0)
+  __shared__ PullArgs A;                   // per-request fields written by CTA 0
+  __shared__ unsigned long long ll[kEngineLLWords];
   __shared__ int go;
-  constexpr unsigned int kPoll = (kEngineLLHeader + 4 * kEnginePollRuns) / 2;   // chunks
-  constexpr unsigned int kPollers = 4;
-  static_assert(kPoll <= 32, "one poll = one warp of 16 B loads");
+  constexpr unsigned int kPoll = (kEngineLLHeader + 4 * kEnginePollRuns) / 2;   // 16 B chunks
+#ifndef KVD_ENGINE_POLLERS
+#define KVD_ENGINE_POLLERS 1
+#endif
+  constexpr unsigned int kPollers = KVD_ENGINE_POLLERS;
+  static_assert(kPoll <= 64, "one poll = one warp, two 16 B loads per lane at most");
   const unsigned int rank = cluster.block_rank();
   const unsigned int ncta = cluster.num_blocks();
   const unsigned int lane = threadIdx.x & 31u;
   const unsigned int warps = blockDim.x >> 5;
   const unsigned int gw = rank * warps + (threadIdx.x >> 5);
   const unsigned int nw = ncta * warps;
-  // the request-independent fields once; per request only the few below
+  // the request-independent fields once; CTA 0 writes the per-request ones
   if (threadIdx.x == 0) A = E.base;
+  unsigned long long t_seen = 0;           // CTA 0, timing: entry validated
   for (unsigned long long k = E.first;; ++k) {
     const unsigned int r = (unsigned int)(k % kEngineRing);
     if (rank == 0) {
       const unsigned long long* L = E.ll + (size_t)r * kEngineLLWords;
       const unsigned long long want = (unsigned long long)(unsigned int)(k + 1);
-      // kPollers warps poll independently, staggered by a fraction of the
-      // PCIe round trip, so an entry is seen ~1 round trip after the host
-      // wrote it rather than ~1.5.  The first warp that validates it copies
-      // its words to shared memory.
+      // kPollers warps poll (staggered by a fraction of the PCIe round trip
+      // when there are several).  One poll reads the header and the first
+      // kEnginePollRuns runs (two 16 B loads per lane at most, both in
+      // flight at once); the first warp that validates it copies its words
+      // to shared memory.  ONE poller is fastest: every poll in flight also
+      // delays the next poll's detection and the publish's system-scope
+      // release (C1 over NVLink, 16 CTAs: 11.9 us host to host with 4
+      // pollers, 9.2 with 2, 8.3 with 1; profiles/r02_engine_pollers.jsonl;
+      // the same in tools/native/pcie_pingpong.cu: 1.55 vs 3.27 us per
+      // host -> device -> host round trip).
       const unsigned int w = threadIdx.x >> 5;
       if (threadIdx.x == 0) go = 0;
       __syncthreads();
       if (w < kPollers) {
         __nanosleep(w * 400);
+        const unsigned int c1 = lane + 32;                 // second chunk of this lane
         for (;;) {
-          unsigned long long x = 0, y = 0;
+          unsigned long long x = 0, y = 0, x1 = 0, y1 = 0;
           if (lane < kPoll) ld_relaxed_sys_v2(L + 2 * lane, x, y);
+          if (c1 < kPoll) ld_relaxed_sys_v2(L + 2 * c1, x1, y1);
           // nruns is word 7 = chunk 3's second word
           const unsigned int nr = (unsigned int)__shfl_sync(0xffffffffu, y, 3);
           const unsigned int need = kEngineLLHeader +
               (nr == kEngineStop ? 0u : 4u * min(nr, kEnginePollRuns));
-          const bool ok = lane >= kPoll ||
-                          ((2 * lane >= need || (x >> 32) == want) &&
-                           (2 * lane + 1 >= need || (y >> 32) == want));
+          const bool ok = (lane >= kPoll || ((2 * lane >= need || (x >> 32) == want) &&
+                                             (2 * lane + 1 >= need || (y >> 32) == want))) &&
+                          (c1 >= kPoll || ((2 * c1 >= need || (x1 >> 32) == want) &&
+                                           (2 * c1 + 1 >= need || (y1 >> 32) == want)));
           const bool all = __all_sync(0xffffffffu, ok);
           if (all && lane == 0 && atomicCAS(&go, 0, 1) == 0) go = 2 + (int)w;   // winner
           __syncwarp();
           const int g = *(volatile int*)&go;
-          if (g == 2 + (int)w && lane < kPoll) {
-            ll[2 * lane] = x;
-            ll[2 * lane + 1] = y;
+          if (g == 2 + (int)w) {
+            if (lane < kPoll) {
+              ll[2 * lane] = x;
+              ll[2 * lane + 1] = y;
+            }
+            if (c1 < kPoll) {
+              ll[2 * c1] = x1;
+              ll[2 * c1 + 1] = y1;
+            }
           }
           if (g) break;
         }
       }
       __syncthreads();
-      const unsigned long long t_seen = globaltimer();
+      t_seen = globaltimer();
       const unsigned int nr = (unsigned int)ll[7];
-      // the descriptor, into every CTA's shared memory
-      for (unsigned int c = 0; c < ncta; ++c) {
-        EngineDesc* Dc = cluster.map_shared_rank(&D, c);
-        if (threadIdx.x == 0) {
-          Dc->token = (ll[0] & 0xffffffffull) | (ll[1] << 32);
-          Dc->request_id = (ll[2] & 0xffffffffull) | (ll[3] << 32);
-          Dc->mbox_pos = (ll[4] & 0xffffffffull) | (ll[5] << 32);
-          Dc->t_seen = t_seen;
-          Dc->slot = (unsigned int)ll[6];
-          Dc->nruns = nr;
-          Dc->tiles_per_lp = (unsigned int)ll[8];
-          Dc->total_tiles = (unsigned int)ll[9];
-          Dc->flags = (unsigned int)ll[10];
+      const unsigned int nwords = nr == kEngineStop ? 0u : 4u * nr;
+      if (nwords > 4 * kEnginePollRuns) {      // beyond the polled runs: wait for each word
+        for (unsigned int q = 4 * kEnginePollRuns + threadIdx.x; q < nwords; q += blockDim.x) {
+          unsigned long long v;
+          do {
+            v = ld_relaxed_sys(L + kEngineLLHeader + q);
+          } while ((v >> 32) != want);
+          ll[kEngineLLHeader + q] = v;
+        }
+        __syncthreads();
+      }
+      // the descriptor into every CTA's shared memory (distributed shared
+      // memory), one remote store per thread: thread c < ncta writes CTA c's
+      // per-request fields, the rest of the threads the run words
+      if (threadIdx.x < ncta) {
+        PullArgs* Ac = cluster.map_shared_rank(&A, threadIdx.x);
+        Ac->nruns = nr;                        // kEngineStop: exit
+        if (nr != kEngineStop) {
+          const unsigned int slot = (unsigned int)ll[6];
+          Ac->token = (ll[0] & 0xffffffffull) | (ll[1] << 32);
+          Ac->request_id = (ll[2] & 0xffffffffull) | (ll[3] << 32);
+          Ac->mbox_pos = (ll[4] & 0xffffffffull) | (ll[5] << 32);
+          Ac->tiles_per_lp = (unsigned int)ll[8];
+          Ac->total_tiles = (unsigned int)ll[9];
+          Ac->flag = E.base.flag + slot;
+          Ac->gt_out = (ll[10] & 1u) ? E.base.gt_out + 4 * (size_t)slot : nullptr;
         }
       }
-      if (nr != kEngineStop) {
-        for (unsigned int q = threadIdx.x; q < 4 * nr; q += blockDim.x) {
-          unsigned long long w;
-          if (q < 4 * kEnginePollRuns) {
-            w = ll[kEngineLLHeader + q];
-          } else {                           // beyond the polled runs: wait for each word
-            do {
-              w = ld_relaxed_sys(L + kEngineLLHeader + q);
-            } while ((w >> 32) != want);
-          }
-          for (unsigned int c = 0; c < ncta; ++c)
-            reinterpret_cast<int*>(cluster.map_shared_rank(&D, c)->runs)[q] = (int)(unsigned int)w;
-        }
+      for (unsigned int i = threadIdx.x; i < ncta * nwords; i += blockDim.x) {
+        const unsigned int c = i / nwords, q = i - c * nwords;
+        reinterpret_cast<int*>(cluster.map_shared_rank(runs, c))[q] =
+            (int)(unsigned int)ll[kEngineLLHeader + q];
       }
     }
-    cluster.sync();                          // D is valid in every CTA
-    if (D.nruns == kEngineStop) return;
+    cluster.sync();                          // the descriptor is valid in every CTA
+    if (A.nruns == kEngineStop) return;
     const unsigned long long t_handed = globaltimer();   // timing: descriptor in every CTA
-    if (threadIdx.x == 0) {
-      A.token = D.token;
-      A.request_id = D.request_id;
-      A.mbox_pos = D.mbox_pos;
-      A.nruns = D.nruns;
-      A.tiles_per_lp = D.tiles_per_lp;
-      A.total_tiles = D.total_tiles;
-      A.flag = E.base.flag + D.slot;
-      A.gt_out = (D.flags & 1u) ? E.base.gt_out + 4 * (size_t)D.slot : nullptr;
-    }
-    __syncthreads();
     for (unsigned int t = gw; t < A.total_tiles; t += nw) {
-      const Tile T = tile_at(A, D.runs, t);
+      const Tile T = tile_at(A, runs, t);
       warp_copy<V, U>(T.dst, T.src, T.bytes, lane);
     }
     // every CTA's tiles landed: the barrier's cluster-scope release/acquire
@@ -945,8 +958,8 @@ engine_kernel(const __grid_constant__ EngineParams E) {
       if (A.gt_out != nullptr) {             // timed: CTA 0 saw the entry -> all tiles landed
         const unsigned long long t1 = globaltimer();
         volatile unsigned long long* o = A.gt_out;
-        o[0] = t1 - D.t_seen;
-        o[1] = D.t_seen;
+        o[0] = t1 - t_seen;
+        o[1] = t_seen;
         o[2] = t_handed;                     // the span's "wait": descriptor handed over
         o[3] = t1;
       }
@@ -954,7 +967,7 @@ engine_kernel(const __grid_constant__ EngineParams E) {
       asm volatile("st.relaxed.sys.global.u64 [%0], %1;" :: "l"(E.done + r), "l"(k + 1)
                    : "memory");
     }
-    // D and A are rewritten for the next request only after the next
+    // A and runs are rewritten for the next request only after the next
     // iteration's poll: every CTA has passed the barrier above by then
   }
 }
