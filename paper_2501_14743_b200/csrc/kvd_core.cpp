@@ -1371,7 +1371,13 @@ static kvd_status launch_shape(const kvd_peer_s* p, Policy& P, kvd::PullArgs& a,
       // the concurrent GEMM keeps 84 % of its throughput (interference sweep).
       const uint64_t avg_tile = std::max<uint64_t>(16, bytes / std::max(1u, a.total_tiles));
       const uint64_t per_cta = (uint64_t)(threads / 32) * (P.stages - 1) * avg_tile;
-      const uint64_t want = ((4608ull << 10) + per_cta - 1) / per_cta;
+      uint64_t want = ((4608ull << 10) + per_cta - 1) / per_cta;
+      // Short requests (<= 48 MiB) are in flight almost whole from the first
+      // ring: twice the pipes ramp up faster and drain a shorter tail (10 MB
+      // C4 shards back to back: 470-488 -> 513-515 GB/s with 96 CTAs; 84 MB:
+      // 708-717 -> 722; 671 MB: no change, profiles/r02_short_sweep.jsonl).
+      // They hold the SMs for tens of microseconds only.
+      if (bytes <= (48ull << 20)) want = std::max<uint64_t>(want, 96);
       max_ctas = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(want, 48), (uint64_t)p->sm_count);
     } else if (P.variant == KVD_VARIANT_TMA) {
       const int per_sm = kvd::pull_ctas_per_sm(P.variant, threads, a.nruns);

@@ -145,6 +145,7 @@ constexpr unsigned int kEngineMaxRuns = 64;        // larger tables take the lau
 constexpr unsigned int kEngineTile = 2048;         // bytes per warp work item
 constexpr unsigned int kEngineThreads = 512;
 constexpr unsigned int kEngineMaxCtas = 16;        // one thread-block cluster (> 8: non-portable)
+constexpr unsigned int kEngineSmemLayers = 128;    // layer-base tables kept in shared memory
 constexpr unsigned int kEngineLLHeader = 12;
 constexpr unsigned int kEngineLLWords = kEngineLLHeader + 4 * kEngineMaxRuns;
 // one poll reads the header and this many runs (two 16 B loads per lane):

@@ -853,8 +853,24 @@ engine_kernel(const __grid_constant__ EngineParams E) {
   const unsigned int warps = blockDim.x >> 5;
   const unsigned int gw = rank * warps + (threadIdx.x >> 5);
   const unsigned int nw = ncta * warps;
-  // the request-independent fields once; CTA 0 writes the per-request ones
-  if (threadIdx.x == 0) A = E.base;
+  // the request-independent fields once; CTA 0 writes the per-request ones.
+  // The layer-base tables of both sides live in shared memory too, so a
+  // tile's address is not a dependent L2 round trip ahead of its data load.
+  __shared__ unsigned long long bases[2][kEngineSmemLayers];
+  const unsigned int NL = E.base.num_layers;
+  const bool smem_bases = NL <= kEngineSmemLayers && E.base.src.table && E.base.dst.table;
+  if (smem_bases)
+    for (unsigned int l = threadIdx.x; l < NL; l += blockDim.x) {
+      bases[0][l] = E.base.src.table[l];
+      bases[1][l] = E.base.dst.table[l];
+    }
+  if (threadIdx.x == 0) {
+    A = E.base;
+    if (smem_bases) {
+      A.src.table = bases[0];
+      A.dst.table = bases[1];
+    }
+  }
   unsigned long long t_seen = 0;           // CTA 0, timing: entry validated
   for (unsigned long long k = E.first;; ++k) {
     const unsigned int r = (unsigned int)(k % kEngineRing);

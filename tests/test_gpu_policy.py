@@ -68,6 +68,23 @@ def test_over_nvlink_uses_tma_ring():
         pair.close()
 
 
+def test_short_nvlink_requests_get_more_ctas():
+    """<= 48 MiB over NVLink: at least 96 CTAs (the request is in flight almost
+    whole from the first ring); longer requests keep the 48-CTA floor."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs")
+    g = kvdgen.C4.with_blocks(256)
+    pair = make_pair(g, g, seed=108, src_dev=0, dst_dev=1)
+    try:
+        for blocks, lo, hi in ((8, 96, 148), (128, 48, 95)):
+            s, d = kvdgen.fragmented_table(blocks, g.num_blocks, g.num_blocks, seed=blocks)
+            info = pull_and_wait(pair, s, d)
+            assert info["variant"] == 4 and lo <= info["ctas"] <= hi, (blocks, info)
+            assert_layers_equal(pair.download_dst(), pair.expected(s, d))
+    finally:
+        pair.close()
+
+
 def test_device_time_globaltimer_cross_check():
     """KVD_OPT_TIMING: the in-kernel %globaltimer span (first CTA start ->
     last CTA done) of each retired single pull, next to the CUDA-event time
