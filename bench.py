@@ -762,7 +762,7 @@ def run_kvd(args, rank, world, local_rank):
     read_ceiling = None
     if peer and multi and args.config != "c1":
         nbytes = min(g.num_layers * (dst.layer_bytes // 32768) * 32768, 2 << 30)
-        read_ceiling = {f"{c}x{st}": peer.calibrate(nbytes, ctas=c, stages=st, reps=3)
+        read_ceiling = {f"{c}x{st}": peer.calibrate(nbytes, ctas=c, stages=st, reps=4)
                         for c in (48, 96, 148) for st in (6, 7)}
 
     base = {}

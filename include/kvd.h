@@ -448,8 +448,9 @@ KVD_API kvd_status kvd_peer_spans(kvd_peer peer, kvd_span* out, uint32_t cap, ui
  * achievable link ceiling (calibration kernel)"): reads `bytes` of the
  * peer's SOURCE cache memory -- layer after layer from each layer's base,
  * contiguous 32 KiB chunks, no block table -- with bulk (TMA) loads into
- * shared memory that are discarded (no stores), `reps` times back to back,
- * and returns bytes * reps / device time (CUDA events) in GB/s (1e9 B/s).
+ * shared memory that are discarded (no stores), `reps` passes in one launch
+ * (after one untimed pass), and returns bytes * reps / device time (CUDA
+ * events) in GB/s (1e9 B/s).
  * That is the most this GPU's SMs can read through the mapping (over NVLink
  * for a peer on another GPU), the ceiling a pull can approach.  `ctas` CTAs
  * of one `stages`-deep ring each (0: one per SM; stages 0: 6).  Synchronous

@@ -2326,11 +2326,13 @@ kvd_status kvd_peer_calibrate(kvd_peer p, uint64_t bytes, uint32_t ctas, uint32_
   float ms = 0;
   cudaError_t e = cudaEventCreate(&e0);
   if (e == cudaSuccess) e = cudaEventCreate(&e1);
-  // one untimed launch (first touch of the mapping, function attributes)
-  if (e == cudaSuccess) e = kvd::launch_calib_read(p->d_src_bases, layer_chunks, total, ctas, stages, s);
+  // one untimed pass (first touch of the mapping, function attributes), then
+  // ONE launch of `reps` passes (its ramp and tail amortised over all of them)
+  if (e == cudaSuccess)
+    e = kvd::launch_calib_read(p->d_src_bases, layer_chunks, total, 1, ctas, stages, s);
   if (e == cudaSuccess) e = cudaEventRecord(e0, s);
-  for (uint32_t r = 0; e == cudaSuccess && r < reps; ++r)
-    e = kvd::launch_calib_read(p->d_src_bases, layer_chunks, total, ctas, stages, s);
+  if (e == cudaSuccess)
+    e = kvd::launch_calib_read(p->d_src_bases, layer_chunks, total, reps, ctas, stages, s);
   if (e == cudaSuccess) e = cudaEventRecord(e1, s);
   if (e == cudaSuccess) e = cudaEventSynchronize(e1);
   if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, e0, e1);

@@ -193,13 +193,14 @@ cudaError_t launch_engine(const EngineParams& params, int variant, unsigned int 
 
 // Link calibration (kvd_peer_calibrate): `ctas` CTAs each run an
 // `stages`-deep ring of kCalibChunk bulk loads over total_chunks chunks of
-// the layers at bases[] (device array; layer_chunks chunks per layer) and
-// discard them.  stages in [1, kCalibMaxStages].
+// the layers at bases[] (device array; layer_chunks chunks per layer),
+// `passes` times in one launch, and discard them.  stages in
+// [1, kCalibMaxStages].
 constexpr unsigned int kCalibChunk = 32768;
 constexpr unsigned int kCalibMaxStages = 7;   // 224 KiB of shared memory
 cudaError_t launch_calib_read(const unsigned long long* bases, unsigned long long layer_chunks,
-                              unsigned long long total_chunks, unsigned int ctas,
-                              unsigned int stages, cudaStream_t stream);
+                              unsigned long long total_chunks, unsigned int passes,
+                              unsigned int ctas, unsigned int stages, cudaStream_t stream);
 
 // Resident CTAs per SM of the pull kernel for the given threads per CTA.
 int pull_ctas_per_sm(int variant, unsigned int threads, unsigned int nruns);

@@ -994,29 +994,33 @@ engine_kernel(const __grid_constant__ EngineParams E) {
 // CTA runs an S-stage ring of kCalibChunk bulk loads from the peer-mapped
 // source layers into shared memory and discards them -- no stores, no block
 // table, no completion -- so the rate is what this GPU's SMs can pull from
-// the mapping at all.  Chunk i of the request is byte (i % layer_chunks) *
-// kCalibChunk of layer i / layer_chunks; CTA c takes chunks c, c + G, ...
+// the mapping at all.  The launch reads the region `passes` times: chunk i
+// is chunk j = i % total_chunks of the region, byte (j % layer_chunks) *
+// kCalibChunk of layer j / layer_chunks; CTA c takes chunks c, c + G, ...
+// (one long launch, so its ramp and tail are a negligible part of it).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(32)
 calib_read_kernel(const unsigned long long* __restrict__ bases, unsigned long long layer_chunks,
-                  unsigned long long total_chunks, unsigned int stages) {
+                  unsigned long long total_chunks, unsigned int passes, unsigned int stages) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint64_t bar[kMaxStages];
   if (threadIdx.x != 0) return;
   for (unsigned int s = 0; s < stages; ++s) mbar_init(&bar[s]);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   auto src = [&](unsigned long long i) {
-    return reinterpret_cast<const char*>(bases[i / layer_chunks] + (i % layer_chunks) * kCalibChunk);
+    const unsigned long long j = i % total_chunks;
+    return reinterpret_cast<const char*>(bases[j / layer_chunks] + (j % layer_chunks) * kCalibChunk);
   };
+  const unsigned long long end = total_chunks * passes;
   unsigned long long next = blockIdx.x;
   unsigned int issued = 0;
-  for (unsigned int s = 0; s < stages && next < total_chunks; ++s, next += gridDim.x, ++issued)
+  for (unsigned int s = 0; s < stages && next < end; ++s, next += gridDim.x, ++issued)
     tma_load(smem + (size_t)s * kCalibChunk, src(next), kCalibChunk, &bar[s]);
   for (unsigned int i = 0; i < issued; ++i) {
     const unsigned int s = i % stages;
     mbar_wait(&bar[s], (i / stages) & 1u);
     // the stage was written by the async proxy and never read: refill at once
-    if (next < total_chunks) {
+    if (next < end) {
       tma_load(smem + (size_t)s * kCalibChunk, src(next), kCalibChunk, &bar[s]);
       next += gridDim.x;
       ++issued;
@@ -1193,13 +1197,13 @@ cudaError_t launch_flag_only(unsigned long long* flag, unsigned long long token,
 }
 
 cudaError_t launch_calib_read(const unsigned long long* bases, unsigned long long layer_chunks,
-                              unsigned long long total_chunks, unsigned int ctas,
-                              unsigned int stages, cudaStream_t stream) {
+                              unsigned long long total_chunks, unsigned int passes,
+                              unsigned int ctas, unsigned int stages, cudaStream_t stream) {
   const size_t smem = (size_t)stages * kCalibChunk;
   cudaError_t e = cudaFuncSetAttribute(calib_read_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
-  calib_read_kernel<<<ctas, 32, smem, stream>>>(bases, layer_chunks, total_chunks, stages);
+  calib_read_kernel<<<ctas, 32, smem, stream>>>(bases, layer_chunks, total_chunks, passes, stages);
   return cudaGetLastError();
 }
 

@@ -76,11 +76,13 @@ def test_short_nvlink_requests_get_more_ctas():
     g = kvdgen.C4.with_blocks(256)
     pair = make_pair(g, g, seed=108, src_dev=0, dst_dev=1)
     try:
+        exp = pair.dst_host
         for blocks, lo, hi in ((8, 96, 148), (128, 48, 95)):
             s, d = kvdgen.fragmented_table(blocks, g.num_blocks, g.num_blocks, seed=blocks)
             info = pull_and_wait(pair, s, d)
             assert info["variant"] == 4 and lo <= info["ctas"] <= hi, (blocks, info)
-            assert_layers_equal(pair.download_dst(), pair.expected(s, d))
+            exp = pair.expected(s, d, exp)          # the second pull lands on the first's result
+            assert_layers_equal(pair.download_dst(), exp)
     finally:
         pair.close()
 

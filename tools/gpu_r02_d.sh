@@ -4,7 +4,7 @@ mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
 TL="timeout 600 python tools/timeline.py --config c4 --tokens 128,1024 --requests 24"
 for e in 0 1 2 3 4 8 0 2 8; do $TL --early $e --label depth$e >> gpurun_out/r02d_tl.jsonl 2>>gpurun_out/r02d_err.log; done
-timeout 600 python tools/small_requests.py --config c4 --tokens 128,1024 --requests 24 --modes single,lib2,batch --no-timing >> gpurun_out/r02d_small.jsonl 2>>gpurun_out/r02d_err.log
+timeout 600 python tools/small_requests.py --config c4 --tokens 128,1024 --requests 24 --modes single,lib2,batch --timing 0 >> gpurun_out/r02d_small.jsonl 2>>gpurun_out/r02d_err.log
 python -c "
 import json
 for l in open('gpurun_out/r02d_tl.jsonl'):

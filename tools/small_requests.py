@@ -53,11 +53,12 @@ def main():
     ap.add_argument("--stages", type=int, default=0)
     ap.add_argument("--ctas", type=int, default=0)
     ap.add_argument("--modes", default="single,batch,merged")
-    ap.add_argument("--no-timing", action="store_true",
-                    help="no KVD_OPT_TIMING events between launches (they break PDL adjacency)")
-    ap.add_argument("--early", type=int, default=1,
-                    help="KVD_OPT_EARLY_LOADS (1 default: the next pull's first ring of source "
-                         "reads overlaps the previous pull's tail)")
+    ap.add_argument("--timing", type=int, default=2, choices=(0, 1, 2),
+                    help="KVD_OPT_TIMING: 2 (default) in-kernel %%globaltimer spans only; 1 also "
+                         "library events around every launch (they break PDL adjacency); 0 off")
+    ap.add_argument("--early", type=int, default=2,
+                    help="KVD_OPT_EARLY_LOADS (the library default, 2: the next pull's first two "
+                         "ring stages of source reads overlap the previous pull's tail)")
     ap.add_argument("--ipc", action="store_true",
                     help="prefill cache in a second process (CUDA IPC mapping, as deployed)")
     a = ap.parse_args()
@@ -96,8 +97,8 @@ def main():
     if a.ctas:
         peer.set(kvd.OPT_MAX_CTAS, a.ctas)
     peer.set(kvd.OPT_EARLY_LOADS, a.early)
-    if not a.no_timing:
-        peer.set(kvd.OPT_TIMING, 1)   # in-kernel %globaltimer spans of single pulls
+    if a.timing:
+        peer.set(kvd.OPT_TIMING, a.timing)   # in-kernel %globaltimer spans of single pulls
     torch.cuda.set_device(a.dst_dev)
     stream = torch.cuda.Stream(a.dst_dev)
     stream2 = torch.cuda.Stream(a.dst_dev)
@@ -160,8 +161,8 @@ def main():
                     times.append(e0.elapsed_time(e1))
             ms = float(np.median(times))
             gt_ms, gt_n = peer.device_time()
-            if not a.no_timing:
-                peer.kernel_time()
+            if a.timing == 1:
+                peer.kernel_time()                 # drop the launch events
             if gt_n:   # mean in-kernel span per request vs the per-request share of the step
                 res[mode + "_kernel_us_per_request"] = round(gt_ms / gt_n * 1e3, 2)
                 res[mode + "_step_us_per_request"] = round(
