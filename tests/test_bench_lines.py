@@ -1,4 +1,4 @@
-"""The committed bench lines (profiles/r01_final_*.json) satisfy the benchmark
+"""The committed bench lines (profiles/r0[12]_final_*.json) satisfy the benchmark
 contract's keys (tools/check_bench_line.py): metric/value/unit, roofline with
 traffic, cpu_baseline at N = 1, e2e with host<->device bytes, gpu_launches,
 clocks without throttle reasons, warm-up >= 3."""
@@ -14,7 +14,7 @@ sys.path.insert(0, os.path.join(ROOT, "tools"))
 
 import check_bench_line  # noqa: E402
 
-FILES = sorted(glob.glob(os.path.join(ROOT, "profiles", "r01_final_*.json")))
+FILES = sorted(glob.glob(os.path.join(ROOT, "profiles", "r0[12]_final_*.json")))
 
 
 @pytest.mark.parametrize("path", FILES, ids=[os.path.basename(p) for p in FILES])
@@ -32,3 +32,4 @@ def test_committed_bench_line_meets_contract(path):
 def test_headline_lines_present():
     names = {os.path.basename(p) for p in FILES}
     assert {"r01_final_n1.json", "r01_final_n2.json", "r01_final_ref.json"} <= names
+    assert {"r02_final_n1.json", "r02_final_n2_c2.json", "r02_final_ref.json"} <= names
