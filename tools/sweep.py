@@ -129,8 +129,11 @@ def main():
         s, d = tables(g, kind, n)
         if var == "tma" and (thr // 32) * st * tile > 225 * 1024:
             continue
-        peer.set(kvd.OPT_VARIANT, VAR[var]).set(kvd.OPT_TILE_BYTES, tile)
-        peer.set(kvd.OPT_THREADS, thr).set(kvd.OPT_MAX_CTAS, ctas).set(kvd.OPT_STAGES, st)
+        if var == "auto":   # the library's own policy (run auto before explicit shapes)
+            peer.set(kvd.OPT_VARIANT, kvd.VARIANT_AUTO)
+        else:
+            peer.set(kvd.OPT_VARIANT, VAR[var]).set(kvd.OPT_TILE_BYTES, tile)
+            peer.set(kvd.OPT_THREADS, thr).set(kvd.OPT_MAX_CTAS, ctas).set(kvd.OPT_STAGES, st)
         for _ in range(a.warmup):
             pull(s, d)
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
