@@ -1,4 +1,4 @@
-"""The N > 1 host path on CPU: world_size-2 (and 4) gloo process groups run
+"""The N > 1 host path on CPU: world_size-2 (and 4, 8) gloo process groups run
 the rail pairing, the one-time blob exchange (Connect()) and the
 max-over-ranks aggregation that bench.py uses on the GPU box.  The blobs
 are synthesised in the documented wire format and decoded by the C ABI's
@@ -75,7 +75,7 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_pairing_exchange_and_aggregation_gloo(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
