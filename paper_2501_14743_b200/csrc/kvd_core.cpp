@@ -1875,6 +1875,9 @@ static kvd_status transfer(kvd_peer p, uint64_t request_id, const int32_t* src_i
     // big run tables go through a per-slot device buffer
     if (a.nruns > kvd::max_param_runs()) {
       if (p->slot_runs_cap[slot] < a.nruns) {
+        // cudaFree / cudaFreeHost synchronise the device: a live engine must
+        // exit first (its watchdog cannot take the mutex we hold)
+        if (p->slot_runs_dev[slot] || p->slot_runs_host[slot]) engine_quiesce(p);
         if (p->slot_runs_dev[slot]) cudaFree(p->slot_runs_dev[slot]);
         if (p->slot_runs_host[slot]) cudaFreeHost(p->slot_runs_host[slot]);
         p->slot_runs_dev[slot] = nullptr;
@@ -2038,6 +2041,9 @@ kvd_status kvd_pull_batch(kvd_peer p, uint32_t num_requests, const uint64_t* req
   DeviceGuard dgd(p->local->device);
   if (!dgd.ok) return fail(KVD_ECUDA, "cannot select device %d", p->local->device);
   if (bi < 0) {
+    // the device-wide synchronise below (and a failed allocation's frees)
+    // would wait for a live engine whose watchdog cannot take our mutex
+    engine_quiesce(p);
     kvd_peer_s::BatchBuf nb;
     nb.cap = std::max<size_t>(bytes_needed, 64 << 10);
     cudaError_t e = cudaMalloc(&nb.dev, C + nb.cap);

@@ -171,3 +171,47 @@ def test_engine_close_while_live():
     finally:
         pair.close()                                       # stops the live engine first
     torch.cuda.synchronize()
+
+
+@pytest.mark.timeout(300, method="thread")
+def test_engine_live_during_device_synchronising_calls():
+    """Calls that synchronise the device under the peer mutex -- the first
+    batched drain (descriptor buffer allocation) and a > 2016-run table
+    outgrowing its slot's device buffer (cudaFree) -- made while the engine
+    is live must stop it first (its idle watchdog cannot take the mutex):
+    before the fix this sequence deadlocked (a 800-seed fuzz soak hung)."""
+    g = kvdgen.CacheGeom(2, 2, 64, 16, 8192, kvdgen.FP16)   # 4 KiB spans
+    pair = _engine_pair(97, 16, g)
+    try:
+        exp = pair.dst_host
+
+        def short():                              # posted to the engine, leaves it live
+            s, d = kvdgen.fragmented_table(8, 8192, 8192, seed=next_request_id() % 1000)
+            rid = next_request_id()
+            pair.peer.pull(rid, s, d)
+            assert pair.peer.info()["launches"] == 0
+            pair.peer.wait(rid)
+            return s, d
+
+        s, d = short()
+        exp = pair.expected(s, d, exp)
+        tables = kvdgen.disjoint_fragmented_tables([40, 24], 8192, 8192, seed=7)
+        rids = [next_request_id() for _ in tables]
+        pair.peer.pull_batch(rids, tables)       # first batch: allocates its buffer
+        for r in rids:
+            pair.peer.wait(r)
+        for s_, d_ in tables:
+            exp = pair.expected(s_, d_, exp)
+        rid = next_request_id()
+        for n in (2100, 2300):                   # the same id -> the same slot, a bigger table
+            s, d = short()
+            exp = pair.expected(s, d, exp)
+            src = np.arange(0, 2 * n, 2, dtype=np.int32)          # every other block: n runs
+            dst = np.arange(1, 2 * n + 1, 2, dtype=np.int32)[::-1].copy()
+            pair.peer.pull(rid, src, dst)
+            assert pair.peer.info()["runs"] == n
+            pair.peer.wait(rid)
+            exp = pair.expected(src, dst, exp)
+        assert_layers_equal(pair.download_dst(), exp)
+    finally:
+        pair.close()

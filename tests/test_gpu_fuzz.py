@@ -1,6 +1,7 @@
-"""Randomised parity: random geometries, layouts, block tables, movers and
-launch shapes -- every pull bit-exact against the oracle, with the in-kernel
-bounds audit on (zero violations).  Seeded, so failures reproduce."""
+"""Randomised parity: random geometries, layouts, block tables, movers,
+launch shapes and the resident engine -- every pull bit-exact against the
+oracle, with the in-kernel bounds audit on (zero violations; the engine's
+posted requests are not audited).  Seeded, so failures reproduce."""
 import os
 import random
 
@@ -61,6 +62,10 @@ def _opts(rng):
         o[kvd.OPT_COALESCE] = 0
     if rng.random() < 0.25:
         o[kvd.OPT_STREAMS] = 2                     # library streams (completion via wait)
+    elif v == kvd.VARIANT_AUTO and rng.random() < 0.3:
+        # the resident engine takes the short requests (<= 2 MiB, <= 64 runs);
+        # the rest still launch, interleaved with the posted ones
+        o[kvd.OPT_ENGINE] = rng.choice([1, 2, 4, 8, 16])
     return o
 
 
