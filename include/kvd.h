@@ -146,8 +146,9 @@ typedef enum {
   KVD_OPT_STAGES = 5,       /* TMA ring depth per pipe, 2..8 (default 4; auto: 6 or 3); pipes * stages *
                                tile_bytes must fit in 225 KiB of shared memory */
   KVD_OPT_AUDIT = 6,        /* 1: every tile checks that it stays inside its layer tensors on
-                               both sides; violations are counted (kvd_peer_audit) and not
-                               copied.  A test/debug mode; 0 (default) off */
+                               both sides (every mover, the resident engine included);
+                               violations are counted (kvd_peer_audit) and not copied.  A
+                               test/debug mode; 0 (default) off */
   KVD_OPT_TIMING = 7,       /* 1: record CUDA events right around every pull kernel on the
                                caller's stream (kvd_peer_kernel_time sums them) and have single
                                pulls measure first-CTA-start -> last-CTA-done with %globaltimer

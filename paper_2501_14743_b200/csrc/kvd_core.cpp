@@ -1621,6 +1621,8 @@ static void engine_post_stop(kvd_peer_s* p) {
 static cudaError_t engine_ensure_live(kvd_peer_s* p) {
   if (p->engine_live) return cudaSuccess;
   p->engine_params.first = p->engine_tail;
+  // KVD_OPT_AUDIT as it is now (changing it stops a live engine first)
+  p->engine_params.base.audit = p->audit_ctr;
   cudaError_t e = kvd::launch_engine(p->engine_params, p->engine_variant, p->engine_ctas,
                                      p->engine_stream);
   if (e == cudaSuccess) p->engine_live = true;

@@ -964,6 +964,10 @@ engine_kernel(const __grid_constant__ EngineParams E) {
     const unsigned long long t_handed = globaltimer();   // timing: descriptor in every CTA
     for (unsigned int t = gw; t < A.total_tiles; t += nw) {
       const Tile T = tile_at(A, runs, t);
+      if (A.audit && !tile_in_bounds(A, T, t)) {          // bounds audit: count, skip
+        if (lane == 0) atomicAdd(A.audit, 1u);
+        continue;
+      }
       warp_copy<V, U>(T.dst, T.src, T.bytes, lane);
     }
     // every CTA's tiles landed: the barrier's cluster-scope release/acquire

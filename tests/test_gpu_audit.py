@@ -1,7 +1,8 @@
 """Bounds audit (KVD_OPT_AUDIT): compute-sanitizer is closed on this pool, so
 every mover checks in-kernel that each tile it copies stays inside its layer
 tensors on both sides.  Here every path -- LSU / LSU32 / TMA / small-request,
-single and batched pulls, push, head slices, padded and folded layouts, ragged
+the resident engine, single and batched pulls, push, head slices, padded and
+folded layouts, ragged
 tiles -- runs with the audit on: zero violations, and the bytes still match
 the oracle."""
 import numpy as np
@@ -23,6 +24,7 @@ CFGS = [
     {kvd.OPT_VARIANT: kvd.VARIANT_TMA, kvd.OPT_TILE_BYTES: 3072, kvd.OPT_STAGES: 3,
      kvd.OPT_THREADS: 64},
     {kvd.OPT_VARIANT: kvd.VARIANT_TMA, kvd.OPT_TILE_BYTES: 16384, kvd.OPT_STAGES: 2},
+    {kvd.OPT_ENGINE: 4},          # single pulls posted to the resident engine
 ]
 
 

@@ -1,7 +1,7 @@
 """Randomised parity: random geometries, layouts, block tables, movers,
 launch shapes and the resident engine -- every pull bit-exact against the
-oracle, with the in-kernel bounds audit on (zero violations; the engine's
-posted requests are not audited).  Seeded, so failures reproduce."""
+oracle, with the in-kernel bounds audit on (zero violations).  Seeded, so
+failures reproduce."""
 import os
 import random
 
