@@ -4,12 +4,14 @@ run concurrently, each request owns its completion slot), and two peers pull
 into one decode cache at the same time.  Destinations are disjoint, so the
 oracle applied in any order gives the expected bytes."""
 import threading
+import time
 
 import numpy as np
 import pytest
 import torch
 
 import kvdgen
+from paper_2501_14743_b200 import kvd
 from gpu_helpers import assert_layers_equal, cache_for, make_pair, next_request_id
 
 pytestmark = pytest.mark.gpu
@@ -307,6 +309,81 @@ def test_batch_slot_reuse_while_batch_runs():
             pair.peer.wait(i)
         exp = pre
         for s, d in t2:
+            exp = pair.expected(s, d, exp)
+        assert_layers_equal(pair.download_dst(), exp)
+    finally:
+        pair.close()
+
+
+@pytest.mark.timeout(300, method="thread")
+@pytest.mark.parametrize("engine", [0, 8])
+def test_threads_mix_pulls_batches_and_polls(engine):
+    """Stress: four issuing threads (single pulls of mixed sizes -- with the
+    resident engine on, the short ones are posted to it and the long ones
+    launched -- and batched drains, on their own streams) while a fifth
+    thread retires completions with kvd_poll_many; a few hundred requests,
+    disjoint destinations, then the whole cache against the oracle."""
+    g = kvdgen.CacheGeom(2, 2, 64, 16, 8192, kvdgen.FP16)   # 4 KiB spans, 16 KiB per block
+    pair = make_pair(g, g, seed=75)
+    try:
+        if engine:
+            pair.peer.set(kvd.OPT_ENGINE, engine)
+        rng = np.random.default_rng(engine)
+        sizes = [int(x) for x in rng.choice([1, 3, 8, 40, 200], 1600,
+                                            p=[0.3, 0.3, 0.25, 0.1, 0.05])]
+        while sum(sizes) > 6500:               # ~80 % of the pool (room for gaps)
+            sizes.pop()
+        tables = kvdgen.disjoint_fragmented_tables(sizes, 8192, 8192, seed=11)
+        ids = [next_request_id() for _ in tables]
+        issued, errors, lock = [], [], threading.Lock()
+
+        def issuer(w):
+            try:
+                stream = torch.cuda.Stream()
+                k = w
+                while k < len(tables):
+                    batch = k % 7 == 3 and k + 4 < len(tables)   # a batch of this thread's next 2
+                    ks = [k, k + 4] if batch else [k]
+                    while True:
+                        try:
+                            if batch:
+                                pair.peer.pull_batch([ids[q] for q in ks],
+                                                     [tables[q] for q in ks], stream)
+                            else:
+                                pair.peer.pull(ids[k], *tables[k], stream)
+                            break
+                        except kvd.KvdError as e:                # all slots in flight
+                            if e.status != kvd.EBUSY:
+                                raise
+                            time.sleep(1e-4)
+                    k += 8 if batch else 4
+                    with lock:
+                        issued.extend(ids[q] for q in ks)
+            except Exception as e:   # pragma: no cover - reported below
+                errors.append(e)
+
+        done = set()
+
+        def poller():
+            try:
+                while len(done) < len(tables) and not errors:
+                    with lock:
+                        pending = [r for r in issued if r not in done]
+                    if pending:
+                        done.update(pair.peer.poll_many(pending))
+            except Exception as e:   # pragma: no cover
+                errors.append(e)
+
+        threads = [threading.Thread(target=issuer, args=(w,)) for w in range(4)]
+        threads.append(threading.Thread(target=poller))
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        assert not errors, errors
+        assert done == set(ids)
+        exp = pair.dst_host
+        for s, d in tables:
             exp = pair.expected(s, d, exp)
         assert_layers_equal(pair.download_dst(), exp)
     finally:
