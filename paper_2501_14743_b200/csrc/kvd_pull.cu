@@ -842,10 +842,7 @@ engine_kernel(const __grid_constant__ EngineParams E) {
   __shared__ unsigned long long ll[kEngineLLWords];
   __shared__ int go;
   constexpr unsigned int kPoll = (kEngineLLHeader + 4 * kEnginePollRuns) / 2;   // 16 B chunks
-#ifndef KVD_ENGINE_POLLERS
-#define KVD_ENGINE_POLLERS 1
-#endif
-  constexpr unsigned int kPollers = KVD_ENGINE_POLLERS;
+  constexpr unsigned int kPollers = 1;      // tools/ab_patches/engine_pollers4.patch: 4
   static_assert(kPoll <= 64, "one poll = one warp, two 16 B loads per lane at most");
   const unsigned int rank = cluster.block_rank();
   const unsigned int ncta = cluster.num_blocks();

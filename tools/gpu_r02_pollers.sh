@@ -4,7 +4,7 @@ python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
 OUT=gpurun_out/r02_engine_pollers.jsonl; : > $OUT
 export KVD_LAT_C1_ONLY=1
 for np in 1 2 4; do
-  bash tools/build_variant.sh pollers$np -DKVD_ENGINE_POLLERS=$np > /dev/null
+  if [ $np = 1 ]; then bash tools/build_variant.sh pollers1 > /dev/null; else sed "s/kPollers = 4;/kPollers = $np;/" tools/ab_patches/engine_pollers4.patch > paper_2501_14743_b200/ab/p$np.patch; bash tools/build_patched.sh pollers$np paper_2501_14743_b200/ab/p$np.patch > /dev/null; fi
   D=$PWD/paper_2501_14743_b200/ab/pollers$np
   nvcc -O2 -I include tools/native/kvd_latency.cu -L $D -lkvd -Xlinker -rpath=$D -o $D/kvd_latency 2>/dev/null
   for rep in 1 2; do
