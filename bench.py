@@ -98,6 +98,10 @@ class ClockSampler:
             self._h = pynvml.nvmlDeviceGetHandleByIndex(phys)
             self._nvml = pynvml
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            # first queries outside the timed region (the first call of each
+            # is the slow one)
+            pynvml.nvmlDeviceGetClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            pynvml.nvmlDeviceGetCurrentClocksEventReasons(self._h)
         except Exception:
             self._nvml = None
         self.period = period_s
@@ -616,11 +620,11 @@ def run_kvd(args, rank, world, local_rank):
         if multi:
             dist.barrier(group=gloo)
 
-    for _ in range(args.warmup):
-        if peer:
-            step()
-    barrier()
-
+    # Everything the timed region needs is set up BEFORE the warm-up (NVML
+    # init can take tens of ms): the GPU goes from the warm-up steps through
+    # the barrier into the timed steps without an idle gap in which its
+    # clocks or links could settle (a gap made the first timed C4 pulls
+    # ~70 us slower in total, profiles/r02_c4_steps.txt).
     K = args.steps
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(K)] if peer and args.timing == "events" else []
@@ -628,11 +632,18 @@ def run_kvd(args, rank, world, local_rank):
     t_end = torch.cuda.Event(enable_timing=True)
     lat_ns = []
     sampler = ClockSampler(dev)
-    launches[0] = 0
     if peer:
         # timer: in-kernel %globaltimer spans only (events between launches would
         # block programmatic dependent launch); events: library events around each launch
         peer.set(kvd.OPT_TIMING, 1 if args.timing == "events" else 2)
+    for _ in range(args.warmup):
+        if peer:
+            step()
+    if peer:                           # the warm-up's spans and events are not the region's
+        peer.device_time()
+        if args.timing == "events":
+            peer.kernel_time()
+    launches[0] = 0
     barrier()
     # Throughput: the K steps are issued back to back, as a serving engine
     # posts each request's pull when it arrives; completions are retired as
