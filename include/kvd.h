@@ -143,8 +143,11 @@ typedef enum {
   KVD_OPT_THREADS = 4,      /* threads per CTA: multiple of 32; LSU 32..512 (default 512);
                                TMA: threads/32 pipes per CTA, 32..256 (default 96 for an
                                explicit TMA variant; the auto policy picks its own) */
-  KVD_OPT_STAGES = 5,       /* TMA ring depth per pipe, 2..8 (default 4; auto: 6 or 3); pipes * stages *
-                               tile_bytes must fit in 225 KiB of shared memory */
+  KVD_OPT_STAGES = 5,       /* TMA ring depth per pipe, 2..8 (default 4; auto: 6 or 3); with an
+                               explicit TMA variant pipes * stages * tile_bytes must fit in
+                               225 KiB of shared memory (KVD_EINVAL otherwise); under AUTO the
+                               library fits THREADS / STAGES / TILE_BYTES to the ring (at most
+                               8 pipes, then fewer stages and pipes) or takes the LSU mover */
   KVD_OPT_AUDIT = 6,        /* 1: every tile checks that it stays inside its layer tensors on
                                both sides (every mover, the resident engine included);
                                violations are counted (kvd_peer_audit) and not copied.  A

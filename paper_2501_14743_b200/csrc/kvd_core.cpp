@@ -1348,15 +1348,28 @@ static kvd_status launch_shape(const kvd_peer_s* p, Policy& P, kvd::PullArgs& a,
       p->threads_set ? p->threads
                      : (P.variant == KVD_VARIANT_TMA ? (P.tma_defaults ? 32u * P.pipes : 96u)
                                                      : (P.small ? 32u : 512u));
+  constexpr uint64_t kRingMax = 225u * 1024u;   // 227 KiB per CTA minus the static mbarriers
+  if (P.variant == KVD_VARIANT_TMA && P.autov) {
+    // AUTO chose the TMA ring: fit the caller's thread / tile / stage options
+    // (set with the LSU mover in mind, e.g. 512 threads) to its shared memory
+    // -- at most 8 pipes, stages down to 2, then fewer pipes -- and if one
+    // pipe's 2-stage ring of this tile still does not fit, take the LSU mover.
+    uint32_t pipes = std::max<uint32_t>(1, std::min<uint32_t>(threads, 256) / 32);
+    auto ring = [&](uint32_t pp) { return (uint64_t)pp * P.stages * a.tile_bytes; };
+    if (!p->stages_set)
+      while (P.stages > 2 && ring(pipes) > kRingMax) --P.stages;
+    while (pipes > 1 && ring(pipes) > kRingMax) --pipes;
+    threads = 32 * pipes;
+    if (ring(pipes) > kRingMax) {
+      P.variant = KVD_VARIANT_LSU;
+      P.tma_defaults = false;
+      threads = p->threads_set ? p->threads : 512u;
+    }
+  }
   if (P.variant == KVD_VARIANT_TMA) {
     if (threads > 256) return fail(KVD_EINVAL, "the TMA mover takes at most 8 pipes (256 threads)");
-    uint64_t smem = (uint64_t)(threads / 32) * P.stages * a.tile_bytes;
-    if (P.tma_defaults && !p->stages_set && smem > 225u * 1024u) {   // auto: shrink the ring
-      P.stages = (uint32_t)std::max<uint64_t>(
-          2, (225u * 1024u) / ((threads / 32) * (uint64_t)a.tile_bytes));
-      smem = (uint64_t)(threads / 32) * P.stages * a.tile_bytes;
-    }
-    if (smem > 225u * 1024u)   // 227 KiB per CTA minus the static mbarriers / flags
+    const uint64_t smem = (uint64_t)(threads / 32) * P.stages * a.tile_bytes;
+    if (smem > kRingMax)   // an explicit TMA variant with options that do not fit
       return fail(KVD_EINVAL, "TMA ring needs %llu B of shared memory (pipes %u x stages %u x "
                   "tile %u); max 225 KiB", (unsigned long long)smem, threads / 32, P.stages,
                   a.tile_bytes);
@@ -1899,6 +1912,7 @@ static kvd_status transfer(kvd_peer p, uint64_t request_id, const int32_t* src_i
     uint32_t threads = 0, ctas = 0;
     s = launch_shape(p, pol, a, info.bytes, &threads, &ctas);
     if (s != KVD_OK) return s;
+    variant = pol.variant;                 // AUTO may have fallen back to the LSU mover
     if (variant == KVD_VARIANT_TMA && !p->row_bytes) {
       a.tile_ctr = p->tile_ctrs + slot;
       // claims of 2 tiles balance short requests best (10 MB: 456 -> 486

@@ -1,12 +1,13 @@
-"""Randomised parity: random geometries, layouts, block tables, movers,
-launch shapes and the resident engine -- every pull bit-exact against the
-oracle, with the in-kernel bounds audit on (zero violations).  Seeded, so
-failures reproduce."""
+"""Randomised parity: random geometries, layouts, cache memory kinds, block
+tables, movers, launch shapes and the resident engine -- every pull
+bit-exact against the oracle, with the in-kernel bounds audit on (zero
+violations).  Seeded, so failures reproduce."""
 import os
 import random
 
 import numpy as np
 import pytest
+import torch
 
 import kvdgen
 from gpu_helpers import assert_layers_equal, make_pair, next_request_id, pull_and_wait
@@ -75,7 +76,16 @@ def test_fuzz_pull(seed):
     rng = random.Random(seed)
     g = _geom(rng)
     dg = g.with_blocks(g.num_blocks + rng.randint(0, 20)) if not any(g.stride) else g
-    pair = make_pair(g, dg, seed=1000 + seed)
+    # caches in torch memory, one allocation per layer or one for all layers,
+    # or in exportable VMM memory (kvd_mem_alloc, §8 f3 groundwork)
+    mem = rng.choice(["torch", "torch", "torch", "single", "vmm"])
+    # on boxes with two GPUs half the cases pull over NVLink (GPU1 <- GPU0:
+    # the TMA ring, early reads and tile claiming of the auto policy)
+    over_link = rng.random() < 0.5 and torch.cuda.device_count() > 1
+    pair = make_pair(g, dg, seed=1000 + seed, single_allocation=mem == "single",
+                     src_memory="vmm" if mem == "vmm" else "torch",
+                     dst_memory="vmm" if mem == "vmm" else "torch",
+                     src_dev=0, dst_dev=1 if over_link else 0)
     try:
         pair.peer.set(kvd.OPT_AUDIT, 1)
         for k, v in _opts(rng).items():

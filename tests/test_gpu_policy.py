@@ -154,3 +154,28 @@ def test_link_calibration_over_nvlink():
         assert 600 < gbs < 900, gbs      # NVLink 5: 900 GB/s per direction on the wire
     finally:
         pair.close()
+
+
+@pytest.mark.parametrize("opts", [{"threads": 512}, {"threads": 256, "tile": 65536},
+                                  {"tile": 131072}, {"threads": 512, "tile": 131072,
+                                                     "stages": 3}])
+def test_auto_over_nvlink_fits_caller_options(opts):
+    """AUTO picks the TMA ring over NVLink; options a caller set with the LSU
+    mover in mind (512 threads, big tiles) are fitted to the ring's shared
+    memory -- fewer pipes or stages, or the LSU mover when one pipe's ring
+    cannot hold two tiles -- instead of failing (a fuzz case did)."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs")
+    from paper_2501_14743_b200 import kvd
+    pair = make_pair(G7B, G7B, seed=109, src_dev=0, dst_dev=1)
+    try:
+        names = {"threads": kvd.OPT_THREADS, "tile": kvd.OPT_TILE_BYTES, "stages": kvd.OPT_STAGES}
+        for k, v in opts.items():
+            pair.peer.set(names[k], v)
+        s, d = kvdgen.fragmented_table(24, G7B.num_blocks, G7B.num_blocks, seed=9)
+        info = pull_and_wait(pair, s, d)
+        if info["variant"] == 4:
+            assert info["threads"] <= 256
+        assert_layers_equal(pair.download_dst(), pair.expected(s, d))
+    finally:
+        pair.close()
