@@ -61,6 +61,8 @@ def _opts(rng):
         o[kvd.OPT_MAX_CTAS] = rng.randint(1, 9)
     if rng.random() < 0.2:
         o[kvd.OPT_COALESCE] = 0
+    if rng.random() < 0.3:
+        o[kvd.OPT_EARLY_LOADS] = rng.choice([0, 1, 3, 8])   # (over NVLink) source reads early
     if rng.random() < 0.25:
         o[kvd.OPT_STREAMS] = 2                     # library streams (completion via wait)
     elif v == kvd.VARIANT_AUTO and rng.random() < 0.3:
@@ -88,8 +90,10 @@ def test_fuzz_pull(seed):
                      src_dev=0, dst_dev=1 if over_link else 0)
     try:
         pair.peer.set(kvd.OPT_AUDIT, 1)
-        for k, v in _opts(rng).items():
+        opts = _opts(rng)
+        for k, v in opts.items():
             pair.peer.set(k, v)
+        rev = None          # the push side (§8 f2): local = prefill cache, imported = decode cache
         exp = pair.dst_host
         for it in range(3):
             n = rng.randint(0, min(g.num_blocks, dg.num_blocks))
@@ -101,7 +105,18 @@ def test_fuzz_pull(seed):
             else:
                 s, d = kvdgen.contiguous_table(n, rng.randint(0, g.num_blocks - n),
                                                rng.randint(0, dg.num_blocks - n))
-            if rng.random() < 0.3 and n > 1:           # batched drain of 2-3 requests
+            op = rng.random()
+            if op < 0.15:                              # push the same table instead
+                if rev is None:
+                    rev = pair.src.open_peer(pair.dst.export())
+                    rev.set(kvd.OPT_AUDIT, 1)
+                    for k, v in opts.items():
+                        if k != kvd.OPT_ENGINE:        # the engine pulls only
+                            rev.set(k, v)
+                rid = next_request_id()
+                rev.push(rid, s, d)
+                rev.wait(rid)
+            elif op < 0.4 and n > 1:                   # batched drain of 2-3 requests
                 cut = sorted(rng.sample(range(1, n), min(2, n - 1)))
                 parts = np.split(np.arange(n), cut)
                 tables = [(s[p], d[p]) for p in parts]
@@ -113,6 +128,10 @@ def test_fuzz_pull(seed):
                 pull_and_wait(pair, s, d)
             exp = pair.expected(s, d, exp)
         assert pair.peer.audit() == 0
+        if rev is not None:
+            assert rev.audit() == 0
         assert_layers_equal(pair.download_dst(), exp)
     finally:
+        if rev is not None:
+            rev.close()
         pair.close()
