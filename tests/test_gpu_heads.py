@@ -1,6 +1,9 @@
 """§8 f4 -- TP-resharding pulls: decode shard j of a TP=4 decode group pulls
 prefill TP=8 shards 2j and 2j+1 into its two head slices.  Expected bytes
 come from the oracle's head-offset element loop (oracle_pull_heads)."""
+import os
+import random
+
 import numpy as np
 import pytest
 import torch
@@ -115,3 +118,61 @@ def test_tp_resharding_tma_rows(hs, hd, nl, batch):
                  variant=kvd.VARIANT_TMA, audit=True)
     if not batch:
         assert all(i["variant"] == kvd.VARIANT_TMA for i in infos)
+
+
+# KVD_FUZZ_SEEDS widens it like tests/test_gpu_fuzz.py
+@pytest.mark.parametrize("seed", range(int(os.environ.get("KVD_FUZZ_SEEDS", "60"))))
+def test_head_slice_fuzz(seed):
+    """Random head-slice pulls (§8 f4): shapes, dtypes, block sizes, head
+    offsets, tables, movers (AUTO / LSU / TMA rows) and ring shapes, single
+    or batched, over NVLink half the time on 2-GPU boxes, bounds audit on --
+    bit-exact against the oracle's head-offset element loop."""
+    rng = random.Random(seed)
+    dt = rng.choice([kvdgen.FP16, kvdgen.BF16, kvdgen.FP8, kvdgen.FP32])
+    e = kvdgen.ELEM_BYTES[dt]
+    nl, d, bs = rng.randint(1, 4), rng.choice([32, 64, 128]), rng.choice([4, 8, 16])
+    hs = rng.choice([1, 2])
+    hd = hs * rng.choice([1, 2, 3, 4])
+    off = rng.randrange(0, hd - hs + 1)
+    nb_s, nb_d = rng.randint(8, 96), rng.randint(8, 96)
+    over_link = rng.random() < 0.5 and torch.cuda.device_count() > 1
+    src = cache_for(kvdgen.CacheGeom(nl, hs, d, bs, nb_s, dt), 0)
+    dst = cache_for(kvdgen.CacheGeom(nl, hd, d, bs, nb_d, dt), 1 if over_link else 0)
+    try:
+        host = _fill(src, 500 + seed)
+        expected = _fill(dst, 900 + seed)
+        torch.cuda.synchronize(0)
+        torch.cuda.synchronize(dst.device)
+        p = dst.open_peer_heads(src.export(), off)
+        p.set(kvd.OPT_AUDIT, 1)
+        v = rng.choice([kvd.VARIANT_AUTO, kvd.VARIANT_LSU, kvd.VARIANT_TMA])
+        p.set(kvd.OPT_VARIANT, v)
+        if v == kvd.VARIANT_TMA and rng.random() < 0.5:
+            p.set(kvd.OPT_THREADS, 32 * rng.choice([1, 2, 4]))
+            p.set(kvd.OPT_STAGES, rng.choice([2, 3]))
+        try:
+            for it in range(3):
+                n = rng.randint(0, min(nb_s, nb_d))
+                table = kvdgen.random_table if rng.random() < 0.5 else kvdgen.fragmented_table
+                s_ids, d_ids = table(n, nb_s, nb_d, seed=seed * 10 + it)
+                if n > 1 and rng.random() < 0.3:
+                    cut = rng.randrange(1, n)
+                    rids = [next_request_id(), next_request_id()]
+                    p.pull_batch(rids, [(s_ids[:cut], d_ids[:cut]), (s_ids[cut:], d_ids[cut:])])
+                    for r in rids:
+                        p.wait(r)
+                else:
+                    rid = next_request_id()
+                    p.pull(rid, s_ids, d_ids)
+                    p.wait(rid)
+                rc = oracle.pull_heads(host, (0,) * 5, nb_s, hs, expected, (0,) * 5, nb_d, hd, off,
+                                       d, bs, e, s_ids, d_ids)
+                assert rc == oracle.OK
+            torch.cuda.synchronize(dst.device)
+            assert p.audit() == 0
+            assert_layers_equal([t.cpu().numpy() for t in dst.layers], expected)
+        finally:
+            p.close()
+    finally:
+        dst.close()
+        src.close()
