@@ -267,12 +267,25 @@ def kvd_peer_set(peer: int, option: int, value: int) -> None:
     _check(_lib.kvd_peer_set(peer, option, int(value)), "kvd_peer_set")
 
 
+_from_buffer = ctypes.c_char.from_buffer
+_addressof = ctypes.addressof
+_I32 = np.dtype(np.int32)
+
+
 def _addr(a: np.ndarray):
-    return a.__array_interface__["data"][0] if a.size else None
+    """Data address of a C-contiguous array (None when empty).  The buffer
+    protocol is ~3x cheaper than __array_interface__ per call, which matters
+    on the per-request path (C1 latency through Python)."""
+    if not a.size:
+        return None
+    try:
+        return _addressof(_from_buffer(a))
+    except (TypeError, ValueError):      # read-only buffer
+        return a.__array_interface__["data"][0]
 
 
 def _ids_fast(a) -> np.ndarray:
-    if type(a) is np.ndarray and a.dtype == np.int32 and a.flags.c_contiguous and a.ndim == 1:
+    if type(a) is np.ndarray and a.dtype is _I32 and a.ndim == 1 and a.flags.c_contiguous:
         return a
     return _ids(a)
 
