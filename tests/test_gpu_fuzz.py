@@ -94,6 +94,7 @@ def test_fuzz_pull(seed):
         for k, v in opts.items():
             pair.peer.set(k, v)
         rev = None          # the push side (§8 f2): local = prefill cache, imported = decode cache
+        pulled = []         # request ids the prefill side must see released (pulls only)
         exp = pair.dst_host
         for it in range(3):
             n = rng.randint(0, min(g.num_blocks, dg.num_blocks))
@@ -124,12 +125,17 @@ def test_fuzz_pull(seed):
                 pair.peer.pull_batch(rids, tables)
                 for r in rids:
                     pair.peer.wait(r)
+                pulled += rids
             else:
-                pull_and_wait(pair, s, d)
+                rid = next_request_id()
+                pull_and_wait(pair, s, d, request_id=rid)
+                pulled.append(rid)
             exp = pair.expected(s, d, exp)
         assert pair.peer.audit() == 0
         if rev is not None:
             assert rev.audit() == 0
+        # Complete() reached the prefill side once per pulled request
+        assert sorted(pair.src.poll_released()) == sorted(pulled)
         assert_layers_equal(pair.download_dst(), exp)
     finally:
         if rev is not None:
