@@ -614,19 +614,34 @@ pull_kernel_tma(const __grid_constant__ PullParams<MAXR> P, unsigned int stages)
     const unsigned int kClaim = a.nreqs ? K : (a.claim ? a.claim : 4u);
     const unsigned int dealt = min(npipes * S, a.total_tiles);
     unsigned int handed = 0, cur = min(pipe * S, dealt), cur_end = min(pipe * S + S, dealt);
-    unsigned int ahead = 0;
+    unsigned int ahead = 0, ahead_n = 0;
     bool have_ahead = false;
+    // guided claiming (single pulls): full claims while plenty remains, single
+    // tiles for the last ~2 claims' worth per pipe, so the pipes finish together
+    const unsigned int guided_tail = a.nreqs ? 0u : npipes * kClaim * 2u;
+    auto claim_n = [&](unsigned int seen) -> unsigned int {
+      return (seen >= a.total_tiles || a.total_tiles - seen > guided_tail) ? kClaim : 1u;
+    };
     auto next = [&]() -> unsigned int {
       if (a.tile_ctr == nullptr) return handed < count ? tile_of(handed++) : kNone;
       if (cur == cur_end) {
-        const unsigned int base = have_ahead ? ahead : dealt + atomicAdd(a.tile_ctr, kClaim);
-        ahead = dealt + atomicAdd(a.tile_ctr, kClaim);   // consumed a block from now
+        unsigned int base, n;
+        if (have_ahead) {
+          base = ahead;
+          n = ahead_n;
+        } else {
+          n = claim_n(cur_end);
+          base = dealt + atomicAdd(a.tile_ctr, n);
+        }
+        ahead_n = claim_n(base + n);
+        ahead = dealt + atomicAdd(a.tile_ctr, ahead_n);   // consumed a block from now
         have_ahead = true;
         if (base >= a.total_tiles) return kNone;
         cur = base;
-        cur_end = min(base + kClaim, a.total_tiles);
+        cur_end = min(base + n, a.total_tiles);
       } else if (!have_ahead && cur + 1 == cur_end) {
-        ahead = dealt + atomicAdd(a.tile_ctr, kClaim);     // ahead of the first dynamic block
+        ahead_n = claim_n(cur_end);
+        ahead = dealt + atomicAdd(a.tile_ctr, ahead_n);   // ahead of the first dynamic block
         have_ahead = true;
       }
       return cur++;
