@@ -182,7 +182,9 @@ typedef enum {
                                drains a ring of request descriptors the host writes into
                                pinned memory (the paper's transaction queue, P:L373-378,
                                posted straight to the device), so a kvd_pull of <= 2 MiB in
-                               <= 64 runs (AUTO variant, not head-sliced) makes no CUDA call and pays no launch latency.  The
+                               <= 64 runs (AUTO variant, not head-sliced) makes no CUDA call
+                               and pays no launch latency (C1 over NVLink: 8.2 us host to
+                               host with 16 CTAs vs 13.4 launched).  The
                                engine is launched on the first such request and exits after
                                2 ms without one (a watchdog thread), so it holds c SMs only
                                while short requests flow.  Such requests are NOT ordered with
@@ -190,7 +192,9 @@ typedef enum {
                                blocks must be free when kvd_pull is called, and completion is
                                observed with kvd_poll_done / kvd_wait_done.  While the engine
                                runs, a device-wide synchronise (cudaDeviceSynchronize) waits up
-                               to the idle timeout; synchronise streams instead.  0 stops it */
+                               to the idle timeout; synchronise streams instead (library calls
+                               that must synchronise the device stop the engine first).  0
+                               stops it */
 } kvd_option;
 
 typedef struct kvd_cache_s* kvd_cache;
