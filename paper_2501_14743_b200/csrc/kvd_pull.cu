@@ -841,12 +841,11 @@ __device__ __forceinline__ void ld_relaxed_sys_v2(const unsigned long long* p, u
 // runs, 16 B LL chunks, one PCIe round trip per poll), validates it from the
 // words' flags and writes the per-request fields and the run table into
 // every CTA's shared memory (DSMEM, one remote store per thread in
-// parallel).  A cluster barrier hands it over (the
-// other CTAs wait there in hardware, they never touch host memory); every
-// CTA copies its tiles, fences its stores, and a second cluster barrier
-// replaces the per-request arrival counter: after it CTA 0 publishes the
-// request with one system-scope release (cumulative over the other CTAs'
-// stores, ordered before it by the barrier's release/acquire).
+// parallel).  A cluster barrier hands it over (the other CTAs wait there in
+// hardware, they never touch host memory); every CTA copies its tiles, and a
+// second cluster barrier replaces the per-request arrival counter: after it
+// CTA 0 publishes the request with one system-scope release (cumulative over
+// the other CTAs' stores, ordered before it by the barrier's release/acquire).
 template <typename V, int U>
 __global__ void __launch_bounds__(kEngineThreads, 1)
 engine_kernel(const __grid_constant__ EngineParams E) {
