@@ -22,6 +22,11 @@
 //             Single pulls hand tiles out dynamically (per-slot counter);
 //             head-sliced peers (§8 f4) have a variant whose stores are
 //             warp-wide strided rows (pull_kernel_tma_rows).
+// Also here: the resident pull engine (engine_kernel, one thread-block
+// cluster draining a descriptor ring in pinned memory, KVD_OPT_ENGINE), the
+// link calibration kernel (calib_read_kernel, discarded bulk reads of the
+// peer cache: the measured read ceiling) and flag_kernel (completion with no
+// bytes).
 // All are bit copies through integer registers / shared memory only (no
 // float type ever touches the data): NaN payloads, -0, subnormals survive.
 // Pull kernels are launched with programmatic stream serialisation
