@@ -141,3 +141,64 @@ def test_fuzz_pull(seed):
         if rev is not None:
             rev.close()
         pair.close()
+
+
+# options a serving loop may change between requests while others are in flight
+_LIVE_OPTS = [(kvd.OPT_STREAMS, [0, 2, 4]), (kvd.OPT_ENGINE, [0, 4, 16]),
+              (kvd.OPT_TIMING, [0, 2]), (kvd.OPT_EARLY_LOADS, [0, 2, 8]),
+              (kvd.OPT_COALESCE, [0, 1]), (kvd.OPT_VARIANT, [kvd.VARIANT_AUTO, kvd.VARIANT_LSU32,
+                                                             kvd.VARIANT_TMA]),
+              (kvd.OPT_MAX_CTAS, [0, 3, 64])]
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("KVD_FUZZ_SEEDS", "200")) // 4))
+def test_fuzz_live_sequence(seed):
+    """A random serving sequence on one peer: single pulls and batched drains
+    left in flight, options changed in between (library streams, the resident
+    engine, timing, early reads, coalescing, mover, grid), completions
+    retired with kvd_poll_many at random points.  Destinations are disjoint
+    across the sequence, so the result is order-free: the whole cache must
+    equal the oracle with every table applied, and the prefill side must see
+    exactly the pulled request ids released."""
+    rng = random.Random(10_000 + seed)
+    g = kvdgen.CacheGeom(rng.randint(1, 3), rng.choice([1, 2, 4]), rng.choice([32, 64, 128]),
+                         rng.choice([8, 16]), 2048, rng.choice([kvdgen.FP16, kvdgen.BF16]))
+    over_link = rng.random() < 0.5 and torch.cuda.device_count() > 1
+    pair = make_pair(g, g, seed=5000 + seed, dst_dev=1 if over_link else 0)
+    try:
+        sizes = [rng.choice([1, 2, 5, 16, 40, 120]) for _ in range(48)]
+        while sum(sizes) > 1500:
+            sizes.pop()
+        tables = kvdgen.disjoint_fragmented_tables(sizes, 2048, 2048, seed=seed)
+        pending, pulled, k = set(), [], 0
+        exp = pair.dst_host
+        while k < len(tables):
+            op = rng.random()
+            if op < 0.2:
+                opt, vals = rng.choice(_LIVE_OPTS)
+                pair.peer.set(opt, rng.choice(vals))
+                continue
+            if op < 0.3 and pending:
+                pending -= set(pair.peer.poll_many(sorted(pending)))
+                continue
+            if op < 0.45 and k + 1 < len(tables):
+                m = min(len(tables) - k, rng.randint(2, 4))
+                rids = [next_request_id() for _ in range(m)]
+                pair.peer.pull_batch(rids, tables[k:k + m])
+                batch = tables[k:k + m]
+                k += m
+            else:
+                rids = [next_request_id()]
+                pair.peer.pull(rids[0], *tables[k])
+                batch = [tables[k]]
+                k += 1
+            pending.update(rids)
+            pulled += rids
+            for s, d in batch:
+                exp = pair.expected(s, d, exp)
+        for r in sorted(pending):
+            pair.peer.wait(r)
+        assert_layers_equal(pair.download_dst(), exp)
+        assert sorted(pair.src.poll_released()) == sorted(pulled)
+    finally:
+        pair.close()
