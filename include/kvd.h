@@ -418,8 +418,9 @@ KVD_API kvd_status kvd_poll_many(kvd_peer peer, const uint64_t* request_ids, uin
 KVD_API kvd_status kvd_peer_audit(kvd_peer peer, uint64_t* violations);
 
 /* Kernel-only device time of the launches recorded since the previous call
- * (KVD_OPT_TIMING): waits for them, returns the summed milliseconds and the
- * number of launches, and forgets them.  KVD_ESTATE if timing is off. */
+ * (KVD_OPT_TIMING = 1; at most 65536 launches are recorded between calls):
+ * waits for them, returns the summed milliseconds and the number of
+ * launches, and forgets them.  KVD_ESTATE if timing is off. */
 KVD_API kvd_status kvd_peer_kernel_time(kvd_peer peer, double* total_ms, uint64_t* launches);
 
 /* In-kernel duration (KVD_OPT_TIMING, single pulls, SURVEY §8 d's

@@ -1486,21 +1486,28 @@ static cudaError_t route_stream(kvd_peer_s* p, cudaStream_t user, cudaStream_t* 
   return cudaSuccess;
 }
 
-static void timing_begin(kvd_peer_s* p, cudaStream_t s) {
-  if (!p->timing_events) return;
+// KVD_OPT_TIMING = 1: an event pair around each launch, kept until
+// kvd_peer_kernel_time reads them -- at most kMaxTimedLaunches between reads
+// (a caller that never reads does not grow them without bound).  Returns
+// whether this launch is bracketed (timing_end only then).
+constexpr size_t kMaxTimedLaunches = 1u << 16;
+static bool timing_begin(kvd_peer_s* p, cudaStream_t s) {
+  if (!p->timing_events || p->timed.size() >= kMaxTimedLaunches) return false;
   std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
   if (!p->event_pool.empty()) {
     ev = p->event_pool.back();
     p->event_pool.pop_back();
   } else if (cudaEventCreate(&ev.first) != cudaSuccess || cudaEventCreate(&ev.second) != cudaSuccess) {
+    if (ev.first) cudaEventDestroy(ev.first);
     cudaGetLastError();
-    return;
+    return false;
   }
   cudaEventRecord(ev.first, s);
   p->timed.push_back(ev);
+  return true;
 }
-static void timing_end(kvd_peer_s* p, cudaStream_t s) {
-  if (p->timing_events && !p->timed.empty()) cudaEventRecord(p->timed.back().second, s);
+static void timing_end(kvd_peer_s* p, cudaStream_t s, bool begun) {
+  if (begun) cudaEventRecord(p->timed.back().second, s);
 }
 
 // ---------------------------------------------------------------------------
@@ -1923,9 +1930,9 @@ static kvd_status transfer(kvd_peer p, uint64_t request_id, const int32_t* src_i
       // the next pull's source reads overlap this one's tail
       a.early_loads = push ? 0u : p->early_loads;
     }
-    timing_begin(p, stream);
+    const bool timed_launch = timing_begin(p, stream);
     e = kvd::launch_pull(a, p->runs4.data(), variant, ctas, threads, pol.stages, stream);
-    timing_end(p, stream);
+    timing_end(p, stream, timed_launch);
     info.launches += 1;
     info.ctas = ctas;
     info.threads = threads;
@@ -2128,9 +2135,9 @@ kvd_status kvd_pull_batch(kvd_peer p, uint32_t num_requests, const uint64_t* req
   if (s != KVD_OK) return s;
   if (pol.variant == KVD_VARIANT_TMA && !p->row_bytes)
     a.tile_ctr = reinterpret_cast<unsigned int*>(B.dev) + 1;   // dynamic tile claiming
-  timing_begin(p, stream);
+  const bool timed_launch = timing_begin(p, stream);
   cudaError_t e = kvd::launch_pull(a, p->runs4.data(), pol.variant, ctas, threads, pol.stages, stream);
-  timing_end(p, stream);
+  timing_end(p, stream, timed_launch);
   if (e != cudaSuccess) return cuda_fail(e, "batched pull launch");
   p->seq += num_requests;
   B.seq += 1;
