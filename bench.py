@@ -517,9 +517,12 @@ def run_kvd(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     dev = local_rank
     multi = world > 1
-    me = cluster.role_of(rank, world)
+    ring = args.pairing == "ring" and multi
+    if ring and not args.no_nccl:
+        args.no_nccl = True            # the NCCL comparators assume prefill/decode halves
+    me = cluster.ring_role_of(rank, world) if ring else cluster.role_of(rank, world)
     role, pairs, half = me.role, me.pairs, world // 2
-    pair_index = (rank % half) if multi else 0
+    pair_index = (rank if ring else rank % half) if multi else 0
     g, reqs, desc = workload(args.config, args.table, pair_index)
     n_req = len(reqs)
     n_blocks = sum(len(s) for s, _ in reqs)
@@ -882,8 +885,12 @@ def run_kvd(args, rank, world, local_rank):
                 "pairs": pairs,
                 "pairing": ("loopback: prefill and decode caches on the same GPU (one GPU has "
                             "no NVLink pair)") if not multi else
-                           f"{pairs}P:{pairs}D rail pairs, rank k -> rank {pairs}+k over NVLink 5",
-                "parallelism": "loopback" if not multi else f"{pairs}x(1P:1D)",
+                           (f"ring stress: every GPU holds both caches and rank k pulls from "
+                            f"rank k+1 mod {world} over NVLink 5 ({pairs} concurrent pulls; "
+                            f"every GPU's ingress and egress carry one)" if ring else
+                            f"{pairs}P:{pairs}D rail pairs, rank k -> rank {pairs}+k over NVLink 5"),
+                "parallelism": ("loopback" if not multi else
+                                f"ring{pairs}" if ring else f"{pairs}x(1P:1D)"),
                 "issue": ("kvd_pull_batch (one launch per step)" if args.batch
                           else "one kvd_pull per request")
                          + (f"; KVD_OPT_STREAMS={args.streams} (consecutive launches overlap "
@@ -1022,6 +1029,10 @@ def main():
                          "streams (completion still polled per request)")
     ap.add_argument("--early", type=int, default=None,
                     help="KVD_OPT_EARLY_LOADS (ring stages read before the preceding pull ends)")
+    ap.add_argument("--pairing", choices=["rail", "ring"], default="rail",
+                    help="rail (default): ranks [0, N/2) prefill, rank k -> N/2 + k; ring: a "
+                         "stress of the switch -- every rank holds both caches and pulls from "
+                         "rank k+1 mod N (N concurrent pulls; no NCCL comparators)")
     ap.add_argument("--memory", choices=["torch", "vmm"], default="torch",
                     help="cache memory: torch/cudaMalloc (legacy IPC) or kvd_mem_alloc (VMM, "
                          "POSIX-fd/fabric handles, §8 f3 groundwork)")

@@ -40,6 +40,20 @@ def role_of(rank: int, world: int) -> Role:
     return Role(rank, world, "decode", rank - half, half)
 
 
+def ring_role_of(rank: int, world: int) -> Role:
+    """A stress of the switch, not the paper's deployment: every rank holds
+    both caches and pulls from its ring successor's prefill cache (rank
+    k <- rank k + 1 mod N), so N pulls run at once and every GPU's NVLink
+    ingress and egress carry one each (full duplex).  With N = 4 that is as
+    many concurrent pulls through NVSwitch as the 4P:4D rail pairing at
+    N = 8.  N = 1 is the loopback."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"rank {rank} of world {world}")
+    if world == 1:
+        return Role(0, 1, "both", 0, 1)
+    return Role(rank, world, "both", (rank + 1) % world, world)
+
+
 def exchange_blobs(blob: Optional[bytes], group=None) -> List[Optional[bytes]]:
     """All ranks contribute their export blob (prefill) or None (decode)."""
     import torch.distributed as dist
@@ -49,8 +63,9 @@ def exchange_blobs(blob: Optional[bytes], group=None) -> List[Optional[bytes]]:
 
 
 def peer_blob(role: Role, blobs: Sequence[Optional[bytes]]) -> Optional[bytes]:
-    """The blob a decode rank opens: its rail partner's."""
-    if role.role != "decode":
+    """The blob a pulling rank opens: its partner's (rail partner, or ring
+    successor)."""
+    if role.role == "prefill":
         return None
     b = blobs[role.peer]
     if b is None:

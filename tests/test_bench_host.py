@@ -63,3 +63,17 @@ def test_pairing_at_every_scaling_point(world):
     for r in roles:                                         # rail rule: k <-> half + k
         assert roles[r.peer].peer == r.rank and abs(r.peer - r.rank) == half
         assert r.pairs == half
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_ring_pairing(world):
+    """bench.py --pairing ring: every rank holds both caches and pulls from
+    its successor, so each rank is pulled from exactly once."""
+    roles = [cluster.ring_role_of(r, world) for r in range(world)]
+    assert all(r.role == "both" for r in roles)
+    if world > 1:
+        assert sorted(r.peer for r in roles) == list(range(world))
+        assert all(r.peer != r.rank for r in roles)
+        blobs = [f"blob{r}".encode() for r in range(world)]
+        assert [cluster.peer_blob(r, blobs) for r in roles] == \
+               [blobs[(r + 1) % world] for r in range(world)]
