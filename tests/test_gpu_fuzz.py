@@ -10,7 +10,9 @@ import pytest
 import torch
 
 import kvdgen
-from gpu_helpers import assert_layers_equal, make_pair, next_request_id, pull_and_wait
+from gpu_helpers import (assert_layers_equal, cache_for, make_pair, next_request_id,
+                         pull_and_wait)
+from oracle import oracle
 from paper_2501_14743_b200 import kvd
 
 pytestmark = pytest.mark.gpu
@@ -202,3 +204,63 @@ def test_fuzz_live_sequence(seed):
         assert sorted(pair.src.poll_released()) == sorted(pulled)
     finally:
         pair.close()
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("KVD_FUZZ_SEEDS", "200")) // 10))
+def test_fuzz_two_exporters_one_decode_cache(seed):
+    """Two prefill caches (one over NVLink on 2-GPU boxes) feed ONE decode
+    cache through two peers whose options -- resident engine, library
+    streams, mover -- are drawn independently, requests interleaved at
+    random and left in flight: per-peer slots, engines and release mailboxes
+    stay separate (each exporter sees exactly its own request ids), and the
+    decode cache equals the oracle with every table applied."""
+    rng = random.Random(20_000 + seed)
+    g = kvdgen.CacheGeom(2, 2, 64, 16, 1024, kvdgen.FP16)
+    two = torch.cuda.device_count() > 1
+    srcs = [cache_for(g, 0), cache_for(g, 1 if two and rng.random() < 0.7 else 0)]
+    dst = cache_for(g, 0)
+    hosts = []
+    for i, c in enumerate(srcs + [dst]):
+        h = [kvdgen.random_bytes(c.layer_bytes, 7000 + 31 * seed + 7 * i + l)
+             for l in range(g.num_layers)]
+        for t, b in zip(c.layers, h):
+            t.copy_(torch.from_numpy(b))
+        hosts.append(h)
+    for c in srcs + [dst]:
+        torch.cuda.synchronize(c.device)
+    peers = [dst.open_peer(c.export()) for c in srcs]
+    try:
+        for p in peers:
+            p.set(kvd.OPT_ENGINE, rng.choice([0, 4, 16]))
+            if rng.random() < 0.3:
+                p.set(kvd.OPT_STREAMS, 2)
+            p.set(kvd.OPT_VARIANT, rng.choice([kvd.VARIANT_AUTO, kvd.VARIANT_AUTO,
+                                               kvd.VARIANT_LSU32, kvd.VARIANT_TMA]))
+        sizes = [rng.choice([1, 3, 8, 24]) for _ in range(40)]
+        tables = kvdgen.disjoint_fragmented_tables(sizes, 1024, 1024, seed=seed)
+        exp = [d.copy() for d in hosts[2]]
+        pulled, inflight = ([], []), []
+        for s, d in tables:
+            i = rng.randrange(2)
+            rid = next_request_id()
+            peers[i].pull(rid, s, d)
+            pulled[i].append(rid)
+            inflight.append((i, rid))
+            rc = oracle.pull(hosts[i], g.stride, g.num_blocks, exp, g.stride, g.num_blocks,
+                             g.num_kv_heads, g.head_dim, g.block_size, g.elem_bytes, s, d)
+            assert rc == oracle.OK
+            if rng.random() < 0.2:
+                for j, r in inflight:
+                    peers[j].wait(r)
+                inflight = []
+        for j, r in inflight:
+            peers[j].wait(r)
+        torch.cuda.synchronize(dst.device)
+        assert_layers_equal([t.cpu().numpy() for t in dst.layers], exp)
+        for i in range(2):
+            assert sorted(srcs[i].poll_released()) == sorted(pulled[i])
+    finally:
+        for p in peers:
+            p.close()
+        for c in srcs + [dst]:
+            c.close()
