@@ -15,7 +15,9 @@ through cudaIpcOpenMemHandle, the peer-mapped source address and the
 cross-process mailbox, only the bytes stay in one HBM -- and (0, 1) over
 NVLink when a second GPU exists.  Each pair runs every scenario in ONE
 prefill/decode process pair (module-scoped fixture); each test asserts its
-own scenario.
+own scenario.  Besides the fixed scenarios, six seeded random serving
+sequences (mover, resident engine, library streams, single pulls and
+batches left in flight, kvd_poll_many) run across the processes too.
 """
 import multiprocessing as mp
 import os
@@ -69,7 +71,7 @@ SCENARIOS = [
     ("heads_auto", "shard0+shard1", AUTO, "heads"),
     ("heads_tma", "shard0+shard1", TMA, "heads"),
     ("engine_short", "small", AUTO, "engine"),
-]
+] + [(f"random{k}", "small", AUTO, f"random{k}") for k in range(6)]
 
 
 def _paths():
@@ -149,6 +151,38 @@ def _scenario(kind, srcs, variant, blobs, dev, rid0):
                                        s, t)
             assert rc == oracle.OK, rc
 
+        if kind.startswith("random"):           # a seeded serving sequence, requests in flight
+            import random
+            rng = random.Random(int(kind[6:]))
+            p0 = peers[0]
+            p0.set(kvd.OPT_VARIANT, rng.choice([AUTO, AUTO, TMA, LSU32]))
+            p0.set(kvd.OPT_ENGINE, rng.choice([0, 8, 16]))
+            p0.set(kvd.OPT_STREAMS, rng.choice([0, 0, 2]))
+            sizes = [rng.choice([1, 2, 6, 20]) for _ in range(30)]
+            while sum(sizes) > 180:             # ~70 % of the 256-block pool (room for gaps)
+                sizes.pop()
+            tables = kvdgen.disjoint_fragmented_tables(sizes, sg.num_blocks, dg.num_blocks,
+                                                       100 + int(kind[6:]))
+            pending, k = set(), 0
+            while k < len(tables):
+                if rng.random() < 0.2 and pending:
+                    pending -= set(p0.poll_many(sorted(pending)))
+                    continue
+                m = rng.choice([1, 1, 1, 2, 3]) if k + 1 < len(tables) else 1
+                m = min(m, len(tables) - k)
+                ids = list(range(rid + 1, rid + 1 + m))
+                rid += m
+                if m == 1:
+                    p0.pull(ids[0], *tables[k])
+                else:
+                    p0.pull_batch(ids, tables[k:k + m])
+                for s, t in tables[k:k + m]:
+                    oracle_pull(names[0], s, t)
+                pending.update(ids)
+                done[names[0]].extend(ids)
+                k += m
+            for r in sorted(pending):
+                p0.wait(r)
         if kind == "engine":                    # short requests through the resident engine
             peers[0].set(kvd.OPT_ENGINE, 8)
             for s, t in kvdgen.disjoint_fragmented_tables([3, 7, 1, 5, 6] * 4, sg.num_blocks,
